@@ -1,0 +1,219 @@
+"""Thin Python binding of libbrng's C ABI (include/brng.h) -- marshalling only.
+
+Every function has the C name and argument order; arrays may be torch
+tensors (device or host), numpy arrays (host) or raw integer addresses.
+Every step of the hot path runs in the CUDA kernels of libbrng.so; there is
+no CPU or PyTorch fallback: if the library cannot be loaded, importing this
+module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbrng.so")
+
+GAMMA_STRIDE = 256
+GAMMA_MAX_TRIAL = 255
+TOTALS_HDR = 16
+TOTALS_LEN = TOTALS_HDR + 256
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libbrng.so not built at {LIB_PATH}: run __graft_entry__.build() "
+                      "(python -m paper_1412_4825_b200._build)")
+_lib = C.CDLL(LIB_PATH)
+
+_u64, _vp, _int = C.c_uint64, C.c_void_p, C.c_int
+_H = C.c_void_p
+
+_SIGS = {
+    "brng_create": [_u64, _u64, C.POINTER(_H)],
+    "brng_destroy": [_H],
+    "brng_set_cuda_stream": [_H, _vp],
+    "brng_get_offset": [_H, C.POINTER(_u64)],
+    "brng_set_offset": [_H, _u64],
+    "brng_get_key": [_H, C.POINTER(_u64), C.POINTER(_u64)],
+    "brng_device_errors": [_H, C.POINTER(_u64)],
+    "brng_reset_device_errors": [_H],
+    "brng_synchronize": [_H],
+    "brng_raw_u32": [_H, _vp, _u64],
+    "brng_std_uniform_f32": [_H, _vp, _u64],
+    "brng_std_uniform_f64": [_H, _vp, _u64],
+    "brng_uniform_f32": [_H, _vp, _vp, _vp, _u64],
+    "brng_uniform_f64": [_H, _vp, _vp, _vp, _u64],
+    "brng_gaussian_f32": [_H, _vp, _vp, _vp, _u64],
+    "brng_gaussian_f64": [_H, _vp, _vp, _vp, _u64],
+    "brng_exponential_f32": [_H, _vp, _vp, _u64],
+    "brng_exponential_f64": [_H, _vp, _vp, _u64],
+    "brng_gamma_f32": [_H, _vp, _vp, _vp, _u64, _vp],
+    "brng_gamma_f64": [_H, _vp, _vp, _vp, _u64, _vp],
+    "brng_dirichlet_f32": [_H, _vp, _u64, _u64, _vp, _vp],
+    "brng_dirichlet_f64": [_H, _vp, _u64, _u64, _vp, _vp],
+    "brng_gibbs_triangle": [_H, _u64, _u64, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp],
+}
+for _name, _args in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _int
+_lib.brng_status_string.argtypes = [_int]
+_lib.brng_status_string.restype = C.c_char_p
+_lib.brng_version.restype = _int
+
+EXPORTED = sorted(list(_SIGS) + ["brng_status_string", "brng_version"])
+
+
+class BrngError(RuntimeError):
+    def __init__(self, fn, status):
+        self.status = status
+        super().__init__(f"{fn}: {brng_status_string(status)} ({status})")
+
+
+def _ptr(x):
+    """torch.Tensor / numpy array / int / None -> address (no copies)."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    dp = getattr(x, "data_ptr", None)
+    if dp is not None:
+        if not x.is_contiguous():
+            raise ValueError("brng: arrays must be contiguous")
+        return dp()
+    ct = getattr(x, "ctypes", None)
+    if ct is not None:
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("brng: arrays must be contiguous")
+        return ct.data
+    raise TypeError(f"brng: unsupported array type {type(x)}")
+
+
+def _check(fn, st):
+    if st != 0:
+        raise BrngError(fn, st)
+    return st
+
+
+def brng_status_string(status: int) -> str:
+    return _lib.brng_status_string(status).decode()
+
+
+def brng_version() -> int:
+    return _lib.brng_version()
+
+
+def brng_create(seed: int, stream_id: int = 0) -> int:
+    h = _H()
+    _check("brng_create", _lib.brng_create(seed, stream_id, C.byref(h)))
+    return h.value
+
+
+def brng_destroy(h) -> int:
+    return _check("brng_destroy", _lib.brng_destroy(h))
+
+
+def brng_set_cuda_stream(h, cuda_stream) -> int:
+    return _check("brng_set_cuda_stream", _lib.brng_set_cuda_stream(h, cuda_stream))
+
+
+def brng_get_offset(h) -> int:
+    v = _u64()
+    _check("brng_get_offset", _lib.brng_get_offset(h, C.byref(v)))
+    return v.value
+
+
+def brng_set_offset(h, cursor: int) -> int:
+    return _check("brng_set_offset", _lib.brng_set_offset(h, cursor))
+
+
+def brng_get_key(h):
+    s, st = _u64(), _u64()
+    _check("brng_get_key", _lib.brng_get_key(h, C.byref(s), C.byref(st)))
+    return s.value, st.value
+
+
+def brng_device_errors(h) -> int:
+    v = _u64()
+    _check("brng_device_errors", _lib.brng_device_errors(h, C.byref(v)))
+    return v.value
+
+
+def brng_reset_device_errors(h) -> int:
+    return _check("brng_reset_device_errors", _lib.brng_reset_device_errors(h))
+
+
+def brng_synchronize(h) -> int:
+    return _check("brng_synchronize", _lib.brng_synchronize(h))
+
+
+def _fill(name, h, n, *arrays):
+    return _check(name, getattr(_lib, name)(h, *[_ptr(a) for a in arrays], n))
+
+
+def brng_raw_u32(h, out, n):
+    return _fill("brng_raw_u32", h, n, out)
+
+
+def brng_std_uniform_f32(h, out, n):
+    return _fill("brng_std_uniform_f32", h, n, out)
+
+
+def brng_std_uniform_f64(h, out, n):
+    return _fill("brng_std_uniform_f64", h, n, out)
+
+
+def brng_uniform_f32(h, a, b, out, n):
+    return _fill("brng_uniform_f32", h, n, a, b, out)
+
+
+def brng_uniform_f64(h, a, b, out, n):
+    return _fill("brng_uniform_f64", h, n, a, b, out)
+
+
+def brng_gaussian_f32(h, mu, sigma, out, n):
+    return _fill("brng_gaussian_f32", h, n, mu, sigma, out)
+
+
+def brng_gaussian_f64(h, mu, sigma, out, n):
+    return _fill("brng_gaussian_f64", h, n, mu, sigma, out)
+
+
+def brng_exponential_f32(h, lam, out, n):
+    return _fill("brng_exponential_f32", h, n, lam, out)
+
+
+def brng_exponential_f64(h, lam, out, n):
+    return _fill("brng_exponential_f64", h, n, lam, out)
+
+
+def brng_gamma_f32(h, alpha, beta, out, n, trials=None):
+    return _check("brng_gamma_f32", _lib.brng_gamma_f32(h, _ptr(alpha), _ptr(beta), _ptr(out),
+                                                        n, _ptr(trials)))
+
+
+def brng_gamma_f64(h, alpha, beta, out, n, trials=None):
+    return _check("brng_gamma_f64", _lib.brng_gamma_f64(h, _ptr(alpha), _ptr(beta), _ptr(out),
+                                                        n, _ptr(trials)))
+
+
+def brng_dirichlet_f32(h, alpha, n_rows, k, out, trials=None):
+    return _check("brng_dirichlet_f32", _lib.brng_dirichlet_f32(h, _ptr(alpha), n_rows, k,
+                                                                _ptr(out), _ptr(trials)))
+
+
+def brng_dirichlet_f64(h, alpha, n_rows, k, out, trials=None):
+    return _check("brng_dirichlet_f64", _lib.brng_dirichlet_f64(h, _ptr(alpha), n_rows, k,
+                                                                _ptr(out), _ptr(trials)))
+
+
+def brng_gibbs_triangle(h, n_chains, n_sweeps, x0=None, y0=None, burn_in=0, out_x=None,
+                        out_y=None, chain_stats=None, final_xy=None, totals=None):
+    return _check("brng_gibbs_triangle", _lib.brng_gibbs_triangle(
+        h, n_chains, n_sweeps, _ptr(x0), _ptr(y0), burn_in, _ptr(out_x), _ptr(out_y),
+        _ptr(chain_stats), _ptr(final_xy), _ptr(totals)))
+
+
+def raw_call(name, *args):
+    """Call any exported symbol with raw arguments and return its status
+    (used by the error-path tests; no checking)."""
+    return getattr(_lib, name)(*args)

@@ -1,0 +1,37 @@
+// brng_internal.h -- launch interface between the C ABI (brng.cpp) and the
+// sm_100a kernels (fill.cu, gamma.cu, gibbs.cu).  Not part of the public ABI.
+#pragma once
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+namespace brng {
+
+enum Dist : int { kRaw = 0, kStdUniform = 1, kUniform = 2, kGaussian = 3, kExponential = 4 };
+enum DType : int { kF32 = 0, kF64 = 1, kU32 = 2 };
+
+struct Ctx {
+  cudaStream_t stream;
+  int num_sms;
+  uint32_t k0, k1;           // Philox key = (lo32 seed, hi32 seed)
+  uint64_t stream_id;        // Philox stream of fills / Gamma / Dirichlet
+  unsigned long long* err;   // device invalid-sample counter
+};
+
+// K1/K2: raw words, standard uniforms and per-sample-parameter transforms.
+cudaError_t launch_fill(int dist, int dtype, const void* p0, const void* p1, void* out,
+                        uint64_t n, uint64_t base, const Ctx& ctx);
+// K3: Marsaglia-Tsang Gamma with warp compaction.
+cudaError_t launch_gamma(int dtype, const void* alpha, const void* beta, void* out,
+                         uint8_t* trials, uint64_t n, uint64_t base, const Ctx& ctx);
+// K4: Dirichlet rows (Gamma + warp-shuffle normalisation).
+cudaError_t launch_dirichlet(int dtype, const void* alpha, uint64_t n_rows, uint64_t k,
+                             void* out, uint8_t* trials, uint64_t base, const Ctx& ctx);
+// K5-K7: Gibbs chains + stats + histogram, then the fixed-order reduction.
+// partials: device scratch of at least gibbs_partials_len(...) doubles.
+size_t gibbs_partials_len(uint64_t n_chains, const Ctx& ctx);
+cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
+                         const double* y0, uint64_t burn_in, double* out_x, double* out_y,
+                         double* chain_stats, double* final_xy, double* totals,
+                         double* partials, uint64_t base, const Ctx& ctx);
+
+}  // namespace brng

@@ -1,0 +1,187 @@
+"""GPU parity of K1/K2 (raw words, standard uniforms, per-sample uniform /
+Gaussian / exponential fills) against the CPU oracle, through the C ABI.
+
+Bit-exact: raw words and standard uniforms.  Tolerance: 2e-6 (f32) / 1e-12
+(f64) relative to the scale of tests/parity.py.  Sizes span many CTAs and a
+ragged tail; misaligned (non-16-byte) pointers take the scalar path; cursors
+cross the 2^32 block boundary; full cfg2 size is checked on sampled windows.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads
+from tests import parity
+from tests.gpu_util import dev, empty, handle, to_dev
+
+pytestmark = pytest.mark.gpu
+
+B = pytest.importorskip("paper_1412_4825_b200") if torch.cuda.is_available() else None
+if B is None:
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+SIZES = [1, 3, 4, 5, 7, 1023, 4099, 100_003]
+CURSORS = [0, 17, (1 << 32) - 5, (1 << 64) - (1 << 20)]
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("cursor", CURSORS)
+def test_raw_u32_bit_exact(n, cursor):
+    for off in (0, 1):
+        with handle(0xDEADBEEF12345678, 0xABCDEF, cursor) as h:
+            out = empty(n, torch.int32, off)
+            B.brng_raw_u32(h, out, n)
+            got = out.cpu().numpy().view(np.uint32)
+            ref = oracle.raw_u32(0xDEADBEEF12345678, 0xABCDEF, cursor, n)
+            assert np.array_equal(got, ref)
+            assert B.brng_get_offset(h) == cursor + (n + 3) // 4
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_std_uniform_bit_exact(n):
+    for off in (0, 1):
+        with handle(99, 5, (1 << 32) - 3) as h:
+            o32 = empty(n, torch.float32, off)
+            B.brng_std_uniform_f32(h, o32, n)
+            o64 = empty(n, torch.float64, off)
+            B.brng_std_uniform_f64(h, o64, n)
+            c2 = (1 << 32) - 3 + (n + 3) // 4
+            assert np.array_equal(o32.cpu().numpy(),
+                                  oracle.std_uniform(99, 5, (1 << 32) - 3, n, np.float32))
+            assert np.array_equal(o64.cpu().numpy(), oracle.std_uniform(99, 5, c2, n, np.float64))
+            assert B.brng_get_offset(h) == c2 + (n + 1) // 2
+
+
+def _params(dist, n, dtype, seed=7):
+    p = workloads.cfg2_params(n, seed=seed)
+    td = torch.float32 if dtype == np.float32 else torch.float64
+    if dist == "uniform":
+        return [p["a"].to(td), p["b"].to(td)]
+    if dist == "gaussian":
+        return [p["mu"].to(td), p["sigma"].to(td)]
+    return [workloads.exp_params(n, seed=seed, dtype=td)]
+
+
+def _call(h, dist, dtype, params, out, n):
+    sfx = "f32" if dtype == np.float32 else "f64"
+    getattr(B, f"brng_{dist}_{sfx}")(h, *params, out, n)
+
+
+@pytest.mark.parametrize("dist", ["uniform", "gaussian", "exponential"])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n", [1, 5, 4099, 100_003])
+def test_fill_parity(dist, dtype, n):
+    td = torch.float32 if dtype == np.float32 else torch.float64
+    for off in (0, 1):
+        params = _params(dist, n, dtype)
+        with handle(7, 0, 1000) as h:
+            dparams = [to_dev(p, off) for p in params]
+            out = empty(n, td, off)
+            _call(h, dist, dtype, dparams, out, n)
+            ref, scale = parity.fill_reference(dist, 7, 0, 1000, [p.numpy() for p in params], 0,
+                                               dtype)
+            parity.check_close(out, ref, scale, dtype, f"{dist} {dtype.__name__} n={n} off={off}")
+            assert B.brng_device_errors(h) == 0
+            per = 2 if dtype == np.float64 else 4
+            assert B.brng_get_offset(h) == 1000 + (n + per - 1) // per
+
+
+def test_chunk_invariance_fills():
+    n = 4096
+    params = _params("gaussian", n, np.float32)
+    d = [p.to(dev()) for p in params]
+    with handle(3) as h:
+        whole = torch.empty(n, device=dev())
+        B.brng_gaussian_f32(h, d[0], d[1], whole, n)
+    with handle(3) as h:
+        a = torch.empty(n, device=dev())
+        B.brng_gaussian_f32(h, d[0][:1000], d[1][:1000], a[:1000], 1000)   # 1000 % 4 == 0
+        B.brng_gaussian_f32(h, d[0][1000:], d[1][1000:], a[1000:], n - 1000)
+    assert torch.equal(whole, a)
+
+
+def test_invalid_parameters_nan_and_counted():
+    a = torch.tensor([0.0, 1.0, float("nan"), 0.0, -float("inf"), 0.0, 0.5], device=dev())
+    b = torch.tensor([1.0, 1.0, 1.0, float("inf"), 0.0, 1.0, 0.25], device=dev())
+    out = torch.empty(7, device=dev())
+    with handle(1) as h:
+        B.brng_uniform_f32(h, a, b, out, 7)
+        assert B.brng_device_errors(h) == 5
+        o = out.cpu().numpy()
+        assert not np.isnan(o[0]) and not np.isnan(o[5])
+        assert np.isnan(o[[1, 2, 3, 4, 6]]).all()
+        B.brng_reset_device_errors(h)
+        mu = torch.zeros(4, dtype=torch.float64, device=dev())
+        sg = torch.tensor([-1.0, 0.0, float("nan"), 2.0], dtype=torch.float64, device=dev())
+        o2 = torch.empty(4, dtype=torch.float64, device=dev())
+        B.brng_gaussian_f64(h, mu, sg, o2, 4)
+        assert B.brng_device_errors(h) == 2
+        assert o2[1].item() == 0.0
+        lam = torch.tensor([0.0, -1.0, 3.0], device=dev())
+        o3 = torch.empty(3, device=dev())
+        B.brng_exponential_f32(h, lam, o3, 3)
+        assert B.brng_device_errors(h) == 4
+
+
+def test_host_buffers_match_device():
+    n = 10_001
+    params = _params("gaussian", n, np.float64)
+    with handle(11) as h:
+        out_h = np.empty(n)
+        B.brng_gaussian_f64(h, params[0].numpy(), params[1].numpy(), out_h, n)
+        c_after = B.brng_get_offset(h)
+    with handle(11) as h:
+        out_d = torch.empty(n, dtype=torch.float64, device=dev())
+        B.brng_gaussian_f64(h, params[0].to(dev()), params[1].to(dev()), out_d, n)
+        assert B.brng_get_offset(h) == c_after
+    assert np.array_equal(out_h, out_d.cpu().numpy())
+
+
+def test_shard_concatenation_equals_whole():
+    # rank r of G processes samples [rN/G, (r+1)N/G) at cursor base + blocks
+    n, G = 1 << 16, 4
+    params = _params("uniform", n, np.float32)
+    d = [p.to(dev()) for p in params]
+    with handle(5) as h:
+        whole = torch.empty(n, device=dev())
+        B.brng_uniform_f32(h, d[0], d[1], whole, n)
+    parts = []
+    for r in range(G):
+        lo, hi = r * n // G, (r + 1) * n // G
+        with handle(5, 0, lo // 4) as h:
+            o = torch.empty(hi - lo, device=dev())
+            B.brng_uniform_f32(h, d[0][lo:hi], d[1][lo:hi], o, hi - lo)
+            parts.append(o)
+    assert torch.equal(torch.cat(parts), whole)
+
+
+@pytest.mark.slow
+def test_cfg2_full_size_sampled():
+    cfg = workloads.CFG2
+    n = cfg["n"]
+    p = workloads.cfg2_params(n, seed=cfg["seed"], device=dev())
+    out_g = torch.empty(n, device=dev())
+    out_u = torch.empty(n, device=dev())
+    with handle(cfg["seed"]) as h:
+        B.brng_gaussian_f32(h, p["mu"], p["sigma"], out_g, n)
+        base_u = B.brng_get_offset(h)
+        B.brng_uniform_f32(h, p["a"], p["b"], out_u, n)
+        assert B.brng_device_errors(h) == 0
+    for lo, hi in parity.windows(n, 48, 512, seed=2):
+        mu, sg = p["mu"][lo:hi].cpu().numpy(), p["sigma"][lo:hi].cpu().numpy()
+        ref, sc = parity.fill_reference("gaussian", cfg["seed"], 0, 0, [mu, sg], lo, np.float32)
+        parity.check_close(out_g[lo:hi], ref, sc, np.float32, f"cfg2 gaussian [{lo},{hi})")
+        a, b = p["a"][lo:hi].cpu().numpy(), p["b"][lo:hi].cpu().numpy()
+        ref, sc = parity.fill_reference("uniform", cfg["seed"], 0, base_u, [a, b], lo, np.float32)
+        parity.check_close(out_u[lo:hi], ref, sc, np.float32, f"cfg2 uniform [{lo},{hi})")
+    # statistics on a deterministic stride subsample of 2^20 (KS, PIT)
+    from tests.stats_util import assert_ks_uniform, pit_normal, pit_uniform
+    idx = torch.arange(0, n, n >> 20, device=dev())
+    assert_ks_uniform(pit_normal(out_g[idx].double().cpu().numpy(),
+                                 p["mu"][idx].double().cpu().numpy(),
+                                 p["sigma"][idx].double().cpu().numpy()), "cfg2 gaussian PIT")
+    a, b = p["a"][idx].cpu().numpy(), p["b"][idx].cpu().numpy()
+    x = out_u[idx].cpu().numpy()
+    assert np.all(x >= a) and np.all(x <= b)
+    assert_ks_uniform(pit_uniform(x, a, b), "cfg2 uniform PIT")
