@@ -1,0 +1,539 @@
+#!/usr/bin/env python3
+"""bench.py -- one JSON line: varying-parameter deviates on B200 (BASELINE.json).
+
+A STEP is one pass of the whole hot path over the five
+BASELINE.json configs at full size, per GPU:
+  cfg1  Gibbs 1024 chains x 1000 sweeps, all samples stored          (K5-K7)
+  cfg2  varying-parameter Gaussian + uniform fills, 2^28 f32 each     (K2)
+  cfg3  varying-alpha Gamma, 2^26 f64                                 (K3)
+  cfg4  LDA-shaped Dirichlet 10^6 x 256 f32                           (K4)
+  cfg5  Gibbs 2^24 chains x 4096 sweeps, per-chain stats + histogram (K5-K7)
+        + the NCCL all-reduce of the totals when N > 1
+A sample is one output deviate (Gibbs: one conditional draw, 2 per sweep;
+Dirichlet: one component).  value = all samples of all ranks / max-over-ranks
+device time.  Weak scaling: rank r draws a disjoint counter range (Gibbs
+streams r*2^24.., fill/Gamma/Dirichlet cursors shifted by r spans), i.e.
+exactly the samples of an N-times larger run.
+
+--impl reference times the CPU oracle (oracle/, the reference arm of this
+tier) on bounded samples of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gsamples/s varying-param Gamma & Gibbs at 1/2/4/8 B200; % of roofline"
+UNIT = "Gsamples/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0          # B200_PROFILING.md fallback
+SMS, SMSP, LANES = 148, 4, 32
+# Algorithmic instruction count per Gibbs sweep:
+# Philox4x32-10 = 10 rounds x (2 IMAD.WIDE + 2 LOP3) = 40; two exact u53
+# conversions 2 x 5 = 10; x,y update 2 DADD + 2 DMUL = 4; statistics 2 DADD +
+# 3 DFMA = 5; histogram bin + ATOMS = 3; loop = 2.  Total 64 issue slots.
+GIBBS_INSTR_PER_SWEEP = 64
+# Per Gamma sample: E[trials] x (Philox 40 + u53 5 + log 30 + sqrt
+# 12 + cospi 25 + test 10) + P(alpha<1) x (Philox 40 + u53 5 + log 30 + div 15
+# + exp 20) + load/store/queue 12 -- evaluated from the measured trial mix.
+GAMMA_TRIAL_INSTR = 122
+GAMMA_BOOST_INSTR = 110
+GAMMA_SAMPLE_INSTR = 12
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, 1965.0, "fallback"
+
+
+# ----------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------
+class Workload:
+    """Inputs resident in HBM, outputs preallocated, one handle per config."""
+
+    def __init__(self, rank, world, torch, B, small=False):
+        import workloads as W
+        self.torch, self.B, self.rank, self.world = torch, B, rank, world
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
+        self.c1, self.c2, self.c3, self.c4, self.c5 = (dict(W.CFG1), dict(W.CFG2), dict(W.CFG3),
+                                                      dict(W.CFG4), dict(W.CFG5))
+        if small:   # quick functional run (--small): not a bench number
+            self.c2["n"] >>= 6; self.c3["n"] >>= 6; self.c4["n_docs"] //= 64
+            self.c5["n_chains"] >>= 6
+        f32, f64 = torch.float32, torch.float64
+        n2, n3 = self.c2["n"], self.c3["n"]
+        D, K = self.c4["n_docs"], self.c4["k"]
+        nc5, ns5 = self.c5["n_chains"], self.c5["n_sweeps"]
+        nc1, ns1 = self.c1["n_chains"], self.c1["n_sweeps"]
+        self.p2 = W.cfg2_params(n2, seed=self.c2["seed"], device=dev)
+        self.p3 = W.cfg3_params(n3, seed=self.c3["seed"], device=dev)
+        self.p4 = W.cfg4_params(D, K, seed=self.c4["seed"], device=dev)
+        self.o2g = torch.empty(n2, dtype=f32, device=dev)
+        self.o2u = torch.empty(n2, dtype=f32, device=dev)
+        self.o3 = torch.empty(n3, dtype=f64, device=dev)
+        self.o4 = torch.empty(D, K, dtype=f32, device=dev)
+        self.o1x = torch.empty(ns1, nc1, dtype=f64, device=dev)
+        self.o1y = torch.empty(ns1, nc1, dtype=f64, device=dev)
+        self.st5 = torch.empty(5, nc5, dtype=f64, device=dev)
+        self.fx5 = torch.empty(2, nc5, dtype=f64, device=dev)
+        self.tot5 = torch.empty(B.TOTALS_LEN, dtype=f64, device=dev)
+        self.tot1 = torch.empty(B.TOTALS_LEN, dtype=f64, device=dev)
+        s = torch.cuda.current_stream().cuda_stream
+        # weak scaling: disjoint counter ranges per rank
+        self.h1 = B.brng_create(self.c1["seed"], rank * nc1)
+        self.h2 = B.brng_create(self.c2["seed"], 0)
+        self.h3 = B.brng_create(self.c3["seed"], 0)
+        self.h4 = B.brng_create(self.c4["seed"], 0)
+        self.h5 = B.brng_create(self.c5["seed"], rank * nc5)
+        for h in (self.h1, self.h2, self.h3, self.h4, self.h5):
+            B.brng_set_cuda_stream(h, s)
+        self.base2 = rank * 2 * ((n2 + 3) // 4)
+        self.base3 = rank * 256 * n3
+        self.base4 = rank * 256 * D * K
+        self.samples = {
+            "cfg1_gibbs": 2 * nc1 * ns1, "cfg2_gaussian": n2, "cfg2_uniform": n2,
+            "cfg3_gamma": n3, "cfg4_dirichlet": D * K, "cfg5_gibbs": 2 * nc5 * ns5,
+        }
+        self.names = list(self.samples)
+        self.launches_per_step = 8 + (0 if world == 1 else 0)
+        self.trials = None
+
+    def reset_cursors(self):
+        B = self.B
+        B.brng_set_offset(self.h1, 0); B.brng_set_offset(self.h2, self.base2)
+        B.brng_set_offset(self.h3, self.base3); B.brng_set_offset(self.h4, self.base4)
+        B.brng_set_offset(self.h5, 0)
+
+    def step(self, ev=None, allreduce=None):
+        """Enqueue one step; ev: dict name -> (start, end) events to record."""
+        B, torch = self.B, self.torch
+        self.reset_cursors()
+        n2, n3 = self.c2["n"], self.c3["n"]
+        D, K = self.c4["n_docs"], self.c4["k"]
+
+        def run(name, fn):
+            if ev is not None:
+                ev[name][0].record()
+            fn()
+            if ev is not None:
+                ev[name][1].record()
+
+        run("cfg1_gibbs", lambda: B.brng_gibbs_triangle(
+            self.h1, self.c1["n_chains"], self.c1["n_sweeps"], None, None, 0, self.o1x,
+            self.o1y, None, None, self.tot1))
+        run("cfg2_gaussian", lambda: B.brng_gaussian_f32(self.h2, self.p2["mu"], self.p2["sigma"],
+                                                         self.o2g, n2))
+        run("cfg2_uniform", lambda: B.brng_uniform_f32(self.h2, self.p2["a"], self.p2["b"],
+                                                       self.o2u, n2))
+        run("cfg3_gamma", lambda: B.brng_gamma_f64(self.h3, self.p3["alpha"], self.p3["beta"],
+                                                   self.o3, n3, self.trials))
+        run("cfg4_dirichlet", lambda: B.brng_dirichlet_f32(self.h4, self.p4, D, K, self.o4, None))
+        run("cfg5_gibbs", lambda: B.brng_gibbs_triangle(
+            self.h5, self.c5["n_chains"], self.c5["n_sweeps"], None, None, 0, None, None,
+            self.st5, self.fx5, self.tot5))
+        if allreduce is not None:
+            allreduce(self.tot5)
+
+    def destroy(self):
+        for h in (self.h1, self.h2, self.h3, self.h4, self.h5):
+            self.B.brng_destroy(h)
+
+
+def gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1412_4825_b200 as B
+
+    hbm_peak, sm_max_cfg, peak_kind = load_peaks()
+    wl = Workload(rank, world, torch, B, small=args.small)
+    allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else None
+    names = wl.names
+    for _ in range(args.warmup):
+        wl.step(allreduce=allreduce)
+    torch.cuda.synchronize()
+
+    # ---- device-timed region ------------------------------------------------
+    evs = [{n: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for n in names} for _ in range(args.steps)]
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for k in range(args.steps):
+        wl.step(ev=evs[k], allreduce=allreduce)
+    t1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = tt.item()
+    ms_step = ms / args.steps
+    per = {n: statistics.mean(e[n][0].elapsed_time(e[n][1]) for e in evs) for n in names}
+    total_samples = sum(wl.samples.values()) * world
+    value = total_samples / (ms_step * 1e-3) / 1e9
+    errs = sum(B.brng_device_errors(h) for h in (wl.h1, wl.h2, wl.h3, wl.h4, wl.h5))
+
+    # ---- roofline of the dominant kernel + breakdown -------------------------
+    sm_hz = (clk.get("sm_max_mhz") or sm_max_cfg) * 1e6
+    issue_peak = SMS * SMSP * LANES * sm_hz            # thread-instructions / s
+    # Gamma trial mix of cfg3, measured once (untimed) from the trials output
+    wl.trials = torch.empty(wl.c3["n"], dtype=torch.uint8, device=wl.dev)
+    B.brng_set_offset(wl.h3, wl.base3)
+    B.brng_gamma_f64(wl.h3, wl.p3["alpha"], wl.p3["beta"], wl.o3, wl.c3["n"], wl.trials)
+    mean_trials = wl.trials.double().mean().item()
+    frac_boost = (wl.p3["alpha"] < 1).double().mean().item()
+    wl.trials = None
+    gamma_instr = (mean_trials * GAMMA_TRIAL_INSTR + frac_boost * GAMMA_BOOST_INSTR
+                   + GAMMA_SAMPLE_INSTR)
+    bd = {}
+    for n in names:
+        t = per[n] * 1e-3
+        d = {"ms": round(per[n], 4), "Gsamples_per_s": round(wl.samples[n] / t / 1e9, 3)}
+        if n in ("cfg2_gaussian", "cfg2_uniform"):
+            gbs = 12.0 * wl.samples[n] / t / 1e9
+            d.update(bound="hbm", GB_per_s=round(gbs, 1), frac=round(gbs / hbm_peak, 4))
+        elif n == "cfg3_gamma":
+            a = gamma_instr * wl.samples[n] / t
+            d.update(bound="alu", frac=round(a / issue_peak, 4), mean_trials=round(mean_trials, 5),
+                     boost_frac=round(frac_boost, 4))
+        elif n in ("cfg1_gibbs", "cfg5_gibbs"):
+            a = GIBBS_INSTR_PER_SWEEP * (wl.samples[n] / 2) / t
+            d.update(bound="alu", frac=round(a / issue_peak, 4),
+                     Gsweeps_per_s=round(wl.samples[n] / 2 / t / 1e9, 3))
+        bd[n] = d
+    dom = max(names, key=lambda n: per[n])
+    t_dom = per[dom] * 1e-3
+    if dom in ("cfg1_gibbs", "cfg5_gibbs"):
+        achieved = GIBBS_INSTR_PER_SWEEP * (wl.samples[dom] / 2) / t_dom / 1e12
+        roof = {"kernel": "gibbs_kernel (" + dom + ")", "bound": "alu",
+                "achieved": round(achieved, 3), "peak": round(issue_peak / 1e12, 3),
+                "unit": "Tinstr/s (issue slots, 148 SM x 4 SMSP x 32 lanes x sm_max clock)",
+                "frac": round(achieved * 1e12 / issue_peak, 4),
+                "algorithmic_per_unit": f"{GIBBS_INSTR_PER_SWEEP} instr/sweep",
+                "traffic": None}
+    else:
+        roof = {"kernel": dom, "bound": bd[dom].get("bound"), "frac": bd[dom].get("frac")}
+    roof["peak_source"] = peak_kind
+
+    # ---- end to end through the C ABI with host buffers ----------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_run(wl, torch, B, args, allreduce, world, dist)
+
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "one step = BASELINE.json configs[0..4] at full size per GPU "
+                               "(cfg1 Gibbs 1024x1000 + cfg2 Gaussian&uniform 2^28 f32 + cfg3 "
+                               "Gamma 2^26 f64 + cfg4 Dirichlet 1e6x256 f32 + cfg5 Gibbs "
+                               "2^24x4096)" + (" [--small: NOT a bench number]" if args.small
+                                               else ""),
+                   "sample_unit": "one output deviate (Gibbs: one conditional draw)",
+                   "samples_per_gpu_step": sum(wl.samples.values()),
+                   "l2": "inputs larger than L2 (each step streams ~9 GB of parameters/outputs)",
+                   "dtypes": {"cfg1": "f64", "cfg2": "f32", "cfg3": "f64", "cfg4": "f32 io, f64 "
+                              "internal", "cfg5": "f64"},
+                   "parallelism": f"dp{world} (disjoint Philox counter ranges)"},
+        "roofline": roof,
+        "breakdown": bd,
+        "gpu_launches": wl.launches_per_step * args.steps,
+        "device_errors": errs,
+        "clocks": clk,
+    }
+    if e2e is not None:
+        out["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.cpu_budget_s)
+    wl.destroy()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e_run(wl, torch, B, args, allreduce, world, dist):
+    """Same step through the C ABI with HOST (pinned) buffers: the library
+    stages host->device, runs the kernels, copies results back (include/brng.h)."""
+    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+    hp2 = {k: pin(v) for k, v in wl.p2.items()}
+    hp3 = {k: pin(v) for k, v in wl.p3.items()}
+    hp4 = pin(wl.p4)
+    o2g, o2u = torch.empty_like(hp2["mu"]).pin_memory(), torch.empty_like(hp2["mu"]).pin_memory()
+    o3 = torch.empty_like(hp3["alpha"]).pin_memory()
+    o4 = torch.empty_like(hp4).pin_memory()
+    c1, c5 = wl.c1, wl.c5
+    o1x = torch.empty(c1["n_sweeps"], c1["n_chains"], dtype=torch.float64).pin_memory()
+    o1y = torch.empty_like(o1x).pin_memory()
+    st5 = torch.empty(5, c5["n_chains"], dtype=torch.float64).pin_memory()
+    fx5 = torch.empty(2, c5["n_chains"], dtype=torch.float64).pin_memory()
+    tot5 = torch.empty(B.TOTALS_LEN, dtype=torch.float64).pin_memory()
+    tot1 = torch.empty(B.TOTALS_LEN, dtype=torch.float64).pin_memory()
+    n2, n3 = wl.c2["n"], wl.c3["n"]
+    D, K = wl.c4["n_docs"], wl.c4["k"]
+
+    def step():
+        wl.reset_cursors()
+        B.brng_gibbs_triangle(wl.h1, c1["n_chains"], c1["n_sweeps"], None, None, 0, o1x, o1y,
+                              None, None, tot1)
+        B.brng_gaussian_f32(wl.h2, hp2["mu"], hp2["sigma"], o2g, n2)
+        B.brng_uniform_f32(wl.h2, hp2["a"], hp2["b"], o2u, n2)
+        B.brng_gamma_f64(wl.h3, hp3["alpha"], hp3["beta"], o3, n3, None)
+        B.brng_dirichlet_f32(wl.h4, hp4, D, K, o4, None)
+        B.brng_gibbs_triangle(wl.h5, c5["n_chains"], c5["n_sweeps"], None, None, 0, None, None,
+                              st5, fx5, tot5)
+        if allreduce is not None:
+            t = tot5.to(wl.dev)
+            allreduce(t)
+            tot5.copy_(t.cpu())
+
+    step()   # warm the stream-ordered pool
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    steps = max(1, min(args.steps, args.e2e_steps))
+    t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(steps):
+        step()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = tt.item()
+    h2d = 4 * n2 * 4 + 2 * n3 * 8 + D * K * 4
+    d2h = 2 * n2 * 4 + n3 * 8 + D * K * 4 + 2 * c1["n_chains"] * c1["n_sweeps"] * 8 + \
+        7 * c5["n_chains"] * 8 + 2 * B.TOTALS_LEN * 8
+    total = sum(wl.samples.values()) * world
+    return {"value": round(total / (ms / steps * 1e-3) / 1e9, 3), "unit": UNIT,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+            "ms_per_step": round(ms / steps, 3)}
+
+
+# ----------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline leg and --impl reference)
+# ----------------------------------------------------------------------------
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_sample_rates(budget_s=15.0, threads=None):
+    """Time the oracle, as it stands, on bounded samples of each config with
+    `threads` workers on disjoint slices.  Returns (rates samples/s per config,
+    description, threads)."""
+    import numpy as np
+    import oracle
+    import workloads as W
+    P = threads or _cores()
+    scale = max(0.05, budget_s / 15.0)
+    rates, desc = {}, []
+
+    def timed(name, n_units, samples_per_unit, fn, chunk):
+        sl = [(lo, min(lo + chunk, n_units)) for lo in range(0, n_units, chunk)]
+        t = time.perf_counter()
+        oracle.run_parallel(fn, sl, P)
+        dt = time.perf_counter() - t
+        rates[name] = n_units * samples_per_unit / dt
+        desc.append(f"{name}: {n_units} units in {dt:.2f}s")
+
+    # cfg2: Gaussian and uniform f32 on the cfg2 parameter recipe
+    n2 = int(2**22 * scale * P / 8) // 4 * 4 or 4
+    p2 = {k: v.numpy() for k, v in W.cfg2_params(n2, seed=7).items()}
+    out = np.empty(n2, np.float32)
+    timed("cfg2_gaussian", n2, 1, lambda lo, hi: oracle.lib().orc_gaussian_f32(
+        7, 0, 0, p2["mu"][lo:].ctypes.data, p2["sigma"][lo:].ctypes.data, out[lo:].ctypes.data,
+        lo, hi - lo), 1 << 16)
+    timed("cfg2_uniform", n2, 1, lambda lo, hi: oracle.lib().orc_uniform_f32(
+        7, 0, 0, p2["a"][lo:].ctypes.data, p2["b"][lo:].ctypes.data, out[lo:].ctypes.data,
+        lo, hi - lo), 1 << 16)
+    # cfg3
+    n3 = int(2**20 * scale * P / 8) or 1
+    p3 = {k: v.numpy() for k, v in W.cfg3_params(n3, seed=11).items()}
+    o3 = np.empty(n3); t3 = np.empty(n3, np.uint8)
+    timed("cfg3_gamma", n3, 1, lambda lo, hi: oracle.lib().orc_gamma_f64(
+        11, 0, 0, p3["alpha"][lo:].ctypes.data, p3["beta"][lo:].ctypes.data, o3[lo:].ctypes.data,
+        t3[lo:].ctypes.data, lo, hi - lo), 1 << 14)
+    # cfg4
+    D = int(2000 * scale * P / 8) or 1
+    a4 = W.cfg4_params(D, 256, seed=3).numpy()
+    o4 = np.empty_like(a4); t4 = np.empty(a4.shape, np.uint8)
+    scratch = [np.empty(256) for _ in range(D)]
+    timed("cfg4_dirichlet", D, 256, lambda lo, hi: oracle.lib().orc_dirichlet_f32(
+        3, 0, 0, a4[lo:].ctypes.data, 256, o4[lo:].ctypes.data, t4[lo:].ctypes.data, lo, hi - lo,
+        scratch[lo].ctypes.data), 64)
+    # cfg5 (and cfg1's per-sweep cost): a stride subset of the 2^24 chains
+    nc = int(2**11 * scale * P / 8) or 1
+    st = np.empty((5, nc)); fx = np.empty((2, nc)); tot = np.zeros((nc, 272))
+
+    def gib(lo, hi):
+        oracle.lib().orc_gibbs_triangle(42, lo, 0, hi - lo, 4096, None, None, 0, None, None,
+                                        None, None, tot[lo].ctypes.data)
+    timed("cfg5_gibbs", nc, 2 * 4096, gib, 16)
+    rates["cfg1_gibbs"] = rates["cfg5_gibbs"]
+    return rates, "; ".join(desc), P
+
+
+def step_samples():
+    import workloads as W
+    return {"cfg1_gibbs": 2 * W.CFG1["n_chains"] * W.CFG1["n_sweeps"],
+            "cfg2_gaussian": W.CFG2["n"], "cfg2_uniform": W.CFG2["n"], "cfg3_gamma": W.CFG3["n"],
+            "cfg4_dirichlet": W.CFG4["n_docs"] * W.CFG4["k"],
+            "cfg5_gibbs": 2 * W.CFG5["n_chains"] * W.CFG5["n_sweeps"]}
+
+
+def projected_value(rates):
+    """Gsamples/s of the full step mix from per-config oracle rates."""
+    s = step_samples()
+    t = sum(s[k] / rates[k] for k in s)
+    return sum(s.values()) / t / 1e9
+
+
+def cpu_baseline(budget_s):
+    rates, desc, P = oracle_sample_rates(budget_s)
+    return {"value": round(projected_value(rates), 6), "unit": UNIT, "cores": P, "kind": "oracle",
+            "sample": "bounded samples of each config on disjoint slices, projected onto the "
+                      "full step mix: " + desc,
+            "per_config_Msamples_per_s": {k: round(v / 1e6, 3) for k, v in rates.items()}}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    budget = args.cpu_budget_s
+    for _ in range(args.warmup):
+        oracle_sample_rates(budget_s=min(budget, 2.0))
+    vals, P, desc, t_total = [], None, "", 0.0
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        rates, desc, P = oracle_sample_rates(budget_s=budget)
+        t_total += time.perf_counter() - t
+        vals.append(projected_value(rates))
+    v = statistics.median(vals)
+    s = step_samples()
+    out = {"metric": METRIC, "value": round(v, 6), "unit": UNIT,
+           "n_gpus": int(os.environ.get("WORLD_SIZE", 1)), "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(sum(s.values()) / (v * 1e9) * 1e3, 3),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "impl": "reference",
+           "config": {"workload": "same step as the GPU arm, timed as bounded samples and "
+                                  "projected (see cpu_baseline.sample)"},
+           "cpu_baseline": {"value": round(v, 6), "unit": UNIT, "cores": P, "kind": "oracle",
+                            "sample": desc},
+           "e2e": {"value": round(v, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0},
+           "wall_s": round(t_total, 2)}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="brng", choices=["brng", "reference"])
+    ap.add_argument("--small", action="store_true", help="1/64 sizes (functional check only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()
