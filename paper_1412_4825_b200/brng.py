@@ -12,7 +12,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbrng.so")
+LIB_PATH = os.environ.get("BRNG_LIB") or os.path.join(_HERE, "libbrng.so")  # BRNG_LIB: tools only
 
 GAMMA_STRIDE = 256
 GAMMA_MAX_TRIAL = 255

@@ -331,7 +331,7 @@ int brng_gibbs_triangle(brng_t h, uint64_t n_chains, uint64_t n_sweeps, const do
                         double* chain_stats, double* final_xy, double* totals) {
   if (!h) return BRNG_ERR_NULL;
   if (burn_in > n_sweeps) return BRNG_ERR_SIZE;
-  if (n_sweeps >= (1ull << 24)) return BRNG_ERR_SIZE;   // u32 shared histogram bound
+  if (n_sweeps >= (1ull << 23)) return BRNG_ERR_SIZE;   // u32 shared histogram bound
   if (n_chains == 0) return BRNG_OK;
   if (!mul_ok(n_chains, n_sweeps) || !mul_ok(n_chains * n_sweeps, 8) || !mul_ok(n_chains, 40))
     return BRNG_ERR_SIZE;

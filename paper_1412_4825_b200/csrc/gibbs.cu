@@ -1,17 +1,31 @@
 // gibbs.cu -- K5/K6/K7: many independent Gibbs chains on the triangle
 // (Eq. 1, Fig. 1):
 //     x ~ U(0, 1-y);  y ~ U(0, 1-x)      from (x0, y0) = (0.5, 0.5)
-// One chain per thread, (x, y) and the running sums in registers; chain c uses
-// Philox stream stream_id + c and sweep s uses block cursor + s (R-15, R-16).
-// Per chain: mean/var of x and y and cov(x,y) over sweeps >= burn_in (R-18);
-// the 256-bin histogram of x goes to a per-CTA shared-memory histogram
-// (R-19).  Per-CTA partials are reduced in a fixed order by a second small
-// kernel, so totals are deterministic for a given launch shape.
+// Chain c uses Philox stream stream_id + c and sweep s uses block cursor + s
+// (R-15, R-16).  Per chain: mean/var of x and y and cov(x,y) over sweeps
+// >= burn_in (R-18); the 256-bin histogram of x goes to a per-CTA shared
+// histogram (R-19).  Per-CTA partials are reduced in a fixed order by a
+// second small kernel, so totals are deterministic for a given launch shape.
 //
-// Only IEEE sub/mul/fma appear in the chain and the statistics, written with
-// explicit round-to-nearest intrinsics so nvcc cannot contract them: the
-// samples, final states, per-chain statistics and histogram are bit-identical
-// to the CPU oracle's.
+// B200 design (measured, tools/ubench.cu + tools/gibbs_lab.cu): the sweep is
+// bound by the FMA-heavy pipe, which executes both the 32x32->64 IMAD.WIDE of
+// Philox (4 cycles/warp) and every fp64 op (2 cycles/warp).  So:
+//   * the parts of Philox that are constant along a chain are hoisted
+//     (17 IMAD.WIDE per block instead of 20; the round-1 product is advanced
+//     with a 64-bit add);
+//   * the chain state is kept SCALED by 2^53: X = x 2^53 = fl(fl(1-y) m) with
+//     m the 53-bit integer of u53 (converted exactly by one I2F.F64.U64 on
+//     the XU pipe), and 1-x = fma(X, -2^-53, 1).  Power-of-two scaling
+//     commutes with IEEE rounding away from under/overflow (values here are
+//     0 or >= 2^-106), so every x, y, sum and fma is bit-identical to the
+//     oracle's unscaled arithmetic while saving the two u53 scalings;
+//   * the histogram bin floor(256 x) = floor(X 2^-45) is read from the bits
+//     of X with integer ops (ALU pipe), not fp64;
+//   * each thread runs two chains interleaved (ILP) with the round keys in
+//     the kernel-parameter constant bank.
+// Only IEEE sub/mul/fma are used, with explicit _rn intrinsics so nvcc cannot
+// contract them: samples, final states, per-chain statistics and histogram are
+// bit-identical to the CPU oracle's.
 #include "brng_internal.h"
 #include "philox.cuh"
 
@@ -19,76 +33,147 @@ namespace brng {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef BRNG_GIBBS_CPT
+#define BRNG_GIBBS_CPT 2
+#endif
+#ifndef BRNG_GIBBS_MINB
+#define BRNG_GIBBS_MINB 2
+#endif
+#ifndef BRNG_GIBBS_UNROLL
+#define BRNG_GIBBS_UNROLL 2
+#endif
+constexpr int kCPT = BRNG_GIBBS_CPT;                      // chains per thread
+constexpr int kUnroll = BRNG_GIBBS_UNROLL;                // sweeps per loop iteration
 constexpr int kHdr = 16;
 constexpr int kTot = kHdr + 256;
+constexpr int kWarps = kThreads / 32;
+constexpr double kTwo53 = 9007199254740992.0;             // 2^53
+constexpr double kTwoM53 = 1.1102230246251565404e-16;     // 2^-53
+constexpr double kTwoM106 = kTwoM53 * kTwoM53;            // 2^-106
 
 struct GibbsArgs {
-  uint64_t n_chains, n_sweeps, burn_in, base, stream_id;
-  uint32_t k0, k1;
-  uint32_t rounds;            // grid-stride rounds per thread
+  uint64_t n_chains, base, stream_id;
+  uint32_t n_sweeps, burn_in;   // n_sweeps < 2^23 (host-checked; u32 histogram)
+  uint32_t rounds;              // grid-stride rounds (kCPT chains per thread each)
+  uint32_t rk0[10], rk1[10];    // Philox round keys k + r*W (kernel constants)
   const double* x0;
   const double* y0;
   double* out_x;
   double* out_y;
   double* chain_stats;
   double* final_xy;
-  double* partials;           // [gridDim.x][kTot]
+  double* partials;             // [gridDim.x][kTot]
   unsigned long long* err;
 };
 
-// floor(256 x) for x in [0, 1): 2^52 + 256 x rounded toward zero keeps the
-// integer part in the low mantissa bits (exact; no F2I conversion).
-__device__ __forceinline__ uint32_t bin256(double x) {
-  return (uint32_t)__double2loint(__fma_rz(x, 256.0, 0x1p52)) & 255u;
+// m = the 53-bit integer of u53(lo, hi) as an exact double (u53 = m 2^-53).
+__device__ __forceinline__ double m53(uint32_t lo, uint32_t hi) {
+  return __ull2double_rn((((uint64_t)hi << 32) | lo) >> 11);
 }
 
-// Philox4x32-10 of block (pos_lo, pos_hi) of a chain's stream with the parts
-// that are invariant along the chain hoisted by the caller:
-//   r1y  = lo(M1 * stream_lo)                     (round 1, word 1)
-//   r1x  = hi(M1 * stream_lo) ^ pos_hi ^ k0       (round 1, word 0)
-//   p0r2 = M0 * r1x                               (round 2, first product)
-//   c3k1 = stream_hi ^ k1
-// Only pos_lo varies per sweep (and it is warp-uniform).
+// floor(256 x) = floor(X 2^-45) for X = x 2^53 in [0, 2^53): with E the
+// unbiased exponent of X, the bin is the top E-44 bits of 1.mantissa, all in
+// the high word; E < 45 (and X = 0) shift everything out (shift >= 21; PTX
+// shr clamps shifts >= 32 to a zero result).
+__device__ __forceinline__ uint32_t bin256_scaled(double X) {
+  const uint32_t h = (uint32_t)__double2hiint(X);
+  const uint32_t sh = 1088u - (h >> 20);                    // 20 - (E - 45)
+  uint32_t b;
+  asm("shr.b32 %0, %1, %2;" : "=r"(b) : "r"((h & 0xFFFFFu) | 0x100000u), "r"(sh));
+  return b;
+}
+
+// Histogram increment at a 32-bit shared-window address (no return value).
+__device__ __forceinline__ void hist_inc(uint32_t saddr) {
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(saddr) : "memory");
+}
+
+// Philox parts constant along a chain segment (stream fixed, high counter
+// word fixed), pre-combined with their round keys so that ptxas keeps them in
+// registers instead of re-deriving them each sweep:
+//   round 1: x = r1x (constant), y = r1y (constant), z = hi(M0 pos_lo) ^ c3k1
+//   round 2: x = hi(M1 z) ^ d2, y = lo(M1 z), z = lo(M0 pos_lo) ^ a2, w = b2
+// with a2 = hi(M0 r1x) ^ k1', b2 = lo(M0 r1x), d2 = r1y ^ k0'.  Per sweep only
+// M0 * pos_lo changes; it is advanced by +M0 (a 64-bit add, no multiply).
 struct ChainKey {
-  uint32_t r1x, r1y, c3k1;
-  uint64_t p0r2;
+  uint32_t c3k1, a2, b2, d2;
 };
 
-__device__ __forceinline__ ChainKey chain_key(uint64_t stream, uint32_t pos_hi, uint32_t k0,
-                                              uint32_t k1) {
+__device__ __forceinline__ ChainKey chain_key(uint64_t stream, uint32_t pos_hi,
+                                              const GibbsArgs& a) {
   ChainKey ck;
   const uint64_t p1 = (uint64_t)kPhiloxM1 * (uint32_t)stream;
-  ck.r1x = (uint32_t)(p1 >> 32) ^ pos_hi ^ k0;
-  ck.r1y = (uint32_t)p1;
-  ck.c3k1 = (uint32_t)(stream >> 32) ^ k1;
-  ck.p0r2 = (uint64_t)kPhiloxM0 * ck.r1x;
+  const uint32_t r1x = (uint32_t)(p1 >> 32) ^ pos_hi ^ a.rk0[0];
+  const uint32_t r1y = (uint32_t)p1;
+  ck.c3k1 = (uint32_t)(stream >> 32) ^ a.rk1[0];
+  const uint64_t p0r2 = (uint64_t)kPhiloxM0 * r1x;
+  ck.a2 = (uint32_t)(p0r2 >> 32) ^ a.rk1[1];
+  ck.b2 = (uint32_t)p0r2;
+  ck.d2 = r1y ^ a.rk0[1];
   return ck;
 }
 
-__device__ __forceinline__ uint4 chain_block(const ChainKey& ck, uint32_t pos_lo, uint32_t k0,
-                                             uint32_t k1) {
-  // round 1
-  const uint64_t p0 = (uint64_t)kPhiloxM0 * pos_lo;
+__device__ __forceinline__ uint4 chain_block(const ChainKey& ck, uint64_t p0, const GibbsArgs& a) {
+  // rounds 1 and 2 (round 1 is free: its products are chain constants or p0)
+  const uint32_t z1 = (uint32_t)(p0 >> 32) ^ ck.c3k1;
+  const uint64_t p1 = (uint64_t)kPhiloxM1 * z1;
   uint4 c;
-  c.x = ck.r1x;
-  c.y = ck.r1y;
-  c.z = (uint32_t)(p0 >> 32) ^ ck.c3k1;
-  c.w = (uint32_t)p0;
-  // round 2 (first product hoisted)
-  {
-    const uint32_t kk0 = k0 + kPhiloxW0, kk1 = k1 + kPhiloxW1;
-    const uint64_t p1 = (uint64_t)kPhiloxM1 * c.z;
-    uint4 r;
-    r.x = (uint32_t)(p1 >> 32) ^ c.y ^ kk0;
-    r.y = (uint32_t)p1;
-    r.z = (uint32_t)(ck.p0r2 >> 32) ^ c.w ^ kk1;
-    r.w = (uint32_t)ck.p0r2;
-    c = r;
-  }
+  c.x = (uint32_t)(p1 >> 32) ^ ck.d2;
+  c.y = (uint32_t)p1;
+  c.z = (uint32_t)p0 ^ ck.a2;
+  c.w = ck.b2;
 #pragma unroll
-  for (int r = 2; r < 10; ++r)
-    c = philox_round(c, k0 + (uint32_t)r * kPhiloxW0, k1 + (uint32_t)r * kPhiloxW1);
+  for (int r = 2; r < 10; ++r) c = philox_round(c, a.rk0[r], a.rk1[r]);
   return c;
+}
+
+// Per-chain state, scaled: X = x 2^53, Y = y 2^53, S1* = s1 2^53,
+// S2*, SXY = s2 2^106.
+struct Chain {
+  double X, Y, S1X, S2X, S1Y, S2Y, SXY;
+  uint64_t c;
+  bool live;     // a real chain with a valid start (stores, histogram)
+};
+
+// Sweeps [s_begin, s_end) of the thread's kCPT chains.
+template <bool STORE, bool STATS>
+__device__ __forceinline__ void sweeps(const GibbsArgs& a, uint32_t s_begin, uint32_t s_end,
+                                       Chain (&ch)[kCPT], uint32_t hist_base) {
+  uint32_t s = s_begin;
+  while (s < s_end) {
+    const uint64_t pos = a.base + s;
+    const uint32_t pos_lo = (uint32_t)pos;
+    const uint64_t room = 0x100000000ull - pos_lo;     // sweeps before lo(pos) wraps
+    const uint32_t e = ((uint64_t)(s_end - s) < room) ? s_end : (uint32_t)(s + room);
+    ChainKey ck[kCPT];
+#pragma unroll
+    for (int k = 0; k < kCPT; ++k)
+      ck[k] = chain_key(a.stream_id + ch[k].c, (uint32_t)(pos >> 32), a);
+    uint64_t p0 = (uint64_t)kPhiloxM0 * pos_lo;
+#pragma unroll kUnroll
+    for (; s < e; ++s) {
+#pragma unroll
+      for (int k = 0; k < kCPT; ++k) {
+        Chain& q = ch[k];
+        const uint4 w = chain_block(ck[k], p0, a);
+        // x = fl(fl(1-y) u53)  <=>  X = fl(fl(1-y) m),  1-y = fma(Y, -2^-53, 1)
+        q.X = __dmul_rn(__fma_rn(q.Y, -kTwoM53, 1.0), m53(w.x, w.y));
+        q.Y = __dmul_rn(__fma_rn(q.X, -kTwoM53, 1.0), m53(w.z, w.w));
+        if (STORE && q.live) {
+          if (a.out_x) a.out_x[(uint64_t)s * a.n_chains + q.c] = __dmul_rn(q.X, kTwoM53);
+          if (a.out_y) a.out_y[(uint64_t)s * a.n_chains + q.c] = __dmul_rn(q.Y, kTwoM53);
+        }
+        if (STATS) {
+          q.S1X = __dadd_rn(q.S1X, q.X); q.S2X = __fma_rn(q.X, q.X, q.S2X);
+          q.S1Y = __dadd_rn(q.S1Y, q.Y); q.S2Y = __fma_rn(q.Y, q.Y, q.S2Y);
+          q.SXY = __fma_rn(q.X, q.Y, q.SXY);
+          // a dead chain (invalid start / padding) counts into bin 256, never read
+          hist_inc(hist_base + 4u * (q.live ? bin256_scaled(q.X) : 256u));
+        }
+      }
+      p0 += kPhiloxM0;
+    }
+  }
 }
 
 __device__ __forceinline__ double warp_sum(double s) {
@@ -97,87 +182,90 @@ __device__ __forceinline__ double warp_sum(double s) {
   return s;
 }
 
-__global__ void __launch_bounds__(kThreads, 4) gibbs_kernel(GibbsArgs a) {
-  __shared__ uint32_t hist[256];
-  __shared__ double red[kThreads / 32][8];
-  __shared__ double tot_s[8][kThreads];        // per-thread chain-level sums
+template <bool STORE>
+__global__ void __launch_bounds__(kThreads, BRNG_GIBBS_MINB) gibbs_kernel(GibbsArgs a) {
+  __shared__ uint32_t hist[257];              // [256] = sink for dead chains
+  __shared__ double red[kWarps][8];
+  const uint32_t hist_base = (uint32_t)__cvta_generic_to_shared(hist);
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   hist[threadIdx.x] = 0;                       // kThreads == 256 bins
-#pragma unroll
-  for (int j = 0; j < 8; ++j) tot_s[j][threadIdx.x] = 0.0;
+  if (lane < 8) red[wid][lane] = 0.0;
   double bins = 0.0;                           // this thread's bin, accumulated
   uint32_t nbad = 0;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  const double n = (double)(a.n_sweeps - a.burn_in);
+  const double nm1 = __dsub_rn(n, 1.0);
   __syncthreads();
 
-  const uint64_t total_threads = (uint64_t)gridDim.x * kThreads;
+  const uint64_t per_round = (uint64_t)gridDim.x * kThreads * kCPT;
   for (uint32_t rnd = 0; rnd < a.rounds; ++rnd) {
-    const uint64_t c = (uint64_t)rnd * total_threads + (uint64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (c < a.n_chains) {
-      double x = a.x0 ? a.x0[c] : 0.5;
-      double y = a.y0 ? a.y0[c] : 0.5;
+    Chain ch[kCPT];
+#pragma unroll
+    for (int k = 0; k < kCPT; ++k) {
+      Chain& q = ch[k];
+      q.c = (uint64_t)rnd * per_round + ((uint64_t)blockIdx.x * kCPT + k) * kThreads +
+            threadIdx.x;
+      const bool real = q.c < a.n_chains;
+      const double x = (real && a.x0) ? a.x0[q.c] : 0.5;
+      const double y = (real && a.y0) ? a.y0[q.c] : 0.5;
       const bool valid = (y >= 0.0) && (y <= 1.0);
-      if (!valid) { x = __longlong_as_double(0x7ff8000000000000ll); y = x; ++nbad; }
-      const uint64_t stream = a.stream_id + c;
-      double s1x = 0.0, s2x = 0.0, s1y = 0.0, s2y = 0.0, sxy = 0.0;
-      uint64_t s = 0;
-      while (s < a.n_sweeps) {
-        // segment of sweeps with a constant high counter word
-        const uint64_t pos = a.base + s;
-        const uint32_t pos_hi = (uint32_t)(pos >> 32);
-        const uint64_t room = 0x100000000ull - (uint32_t)pos;
-        const uint64_t seg_end = (a.n_sweeps - s < room) ? a.n_sweeps : s + room;
-        const ChainKey ck = chain_key(stream, pos_hi, a.k0, a.k1);
-        for (; s < seg_end; ++s) {
-          const uint4 w = chain_block(ck, (uint32_t)(a.base + s), a.k0, a.k1);
-          x = __dmul_rn(__dsub_rn(1.0, y), u53(w.x, w.y));   // x ~ U(0, 1-y)
-          y = __dmul_rn(__dsub_rn(1.0, x), u53(w.z, w.w));   // y ~ U(0, 1-x)
-          if (a.out_x) a.out_x[s * a.n_chains + c] = x;
-          if (a.out_y) a.out_y[s * a.n_chains + c] = y;
-          if (s >= a.burn_in) {
-            s1x = __dadd_rn(s1x, x); s2x = fma(x, x, s2x);
-            s1y = __dadd_rn(s1y, y); s2y = fma(y, y, s2y);
-            sxy = fma(x, y, sxy);
-            if (valid) atomicAdd(&hist[bin256(x)], 1u);
-          }
-        }
-      }
-      const double n = (double)(a.n_sweeps - a.burn_in);
-      const double nm1 = __dsub_rn(n, 1.0);
+      q.live = real && valid;
+      nbad += (real && !valid);
+      q.X = __dmul_rn(x, kTwo53);
+      q.Y = __dmul_rn(valid ? y : qnan, kTwo53);
+      q.S1X = q.S2X = q.S1Y = q.S2Y = q.SXY = 0.0;
+    }
+    sweeps<STORE, false>(a, 0, a.burn_in, ch, hist_base);
+    sweeps<STORE, true>(a, a.burn_in, a.n_sweeps, ch, hist_base);
+
+    double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < kCPT; ++k) {
+      const Chain& q = ch[k];
+      if (q.c >= a.n_chains) continue;
+      const double s1x = __dmul_rn(q.S1X, kTwoM53), s1y = __dmul_rn(q.S1Y, kTwoM53);
+      const double s2x = __dmul_rn(q.S2X, kTwoM106), s2y = __dmul_rn(q.S2Y, kTwoM106);
+      const double sxy = __dmul_rn(q.SXY, kTwoM106);
       const double mx = __ddiv_rn(s1x, n), my = __ddiv_rn(s1y, n);
       const double vx = __ddiv_rn(__dsub_rn(s2x, __dmul_rn(s1x, mx)), nm1);
       const double vy = __ddiv_rn(__dsub_rn(s2y, __dmul_rn(s1y, my)), nm1);
       const double cxy = __ddiv_rn(__dsub_rn(sxy, __dmul_rn(s1x, my)), nm1);
+      const double fx = __dmul_rn(q.X, kTwoM53), fy = __dmul_rn(q.Y, kTwoM53);
       if (a.chain_stats) {
-        a.chain_stats[0 * a.n_chains + c] = mx;
-        a.chain_stats[1 * a.n_chains + c] = vx;
-        a.chain_stats[2 * a.n_chains + c] = my;
-        a.chain_stats[3 * a.n_chains + c] = vy;
-        a.chain_stats[4 * a.n_chains + c] = cxy;
+        a.chain_stats[0 * a.n_chains + q.c] = mx;
+        a.chain_stats[1 * a.n_chains + q.c] = vx;
+        a.chain_stats[2 * a.n_chains + q.c] = my;
+        a.chain_stats[3 * a.n_chains + q.c] = vy;
+        a.chain_stats[4 * a.n_chains + q.c] = cxy;
       }
-      if (a.final_xy) { a.final_xy[c] = x; a.final_xy[a.n_chains + c] = y; }
-      double* t = &tot_s[0][threadIdx.x];
-      t[0 * kThreads] += mx; t[1 * kThreads] += vx; t[2 * kThreads] += mx * mx;
-      t[3 * kThreads] += my; t[4 * kThreads] += vy; t[5 * kThreads] += my * my;
-      t[6 * kThreads] += cxy; t[7 * kThreads] += mx * my;
+      if (a.final_xy) { a.final_xy[q.c] = fx; a.final_xy[a.n_chains + q.c] = fy; }
+      if (STORE && !q.live) {             // invalid start: NaN samples (oracle semantics)
+        for (uint32_t s = 0; s < a.n_sweeps; ++s) {
+          if (a.out_x) a.out_x[(uint64_t)s * a.n_chains + q.c] = qnan;
+          if (a.out_y) a.out_y[(uint64_t)s * a.n_chains + q.c] = qnan;
+        }
+      }
+      t[0] += mx; t[1] += vx; t[2] += mx * mx; t[3] += my; t[4] += vy; t[5] += my * my;
+      t[6] += cxy; t[7] += mx * my;
     }
-    // drain the u32 shared histogram every round (<= 256 * n_sweeps counts)
+    // fixed-order reduction of this round's chain-level sums (warp tree, then
+    // lane 0 accumulates across rounds in order)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double v = warp_sum(t[j]);
+      if (lane == 0) red[wid][j] += v;
+    }
+    // drain the u32 shared histogram every round (< 512 * 2^23 = 2^32 counts)
     __syncthreads();
     bins += (double)hist[threadIdx.x];
     hist[threadIdx.x] = 0;
     __syncthreads();
   }
 
-  // fixed-order CTA reduction of the 8 chain-level sums
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const double v = warp_sum(tot_s[j][threadIdx.x]);
-    if (lane == 0) red[wid][j] = v;
-  }
-  __syncthreads();
   double* part = a.partials + (uint64_t)blockIdx.x * kTot;
   if (threadIdx.x < 8) {
     double v = 0.0;
-    for (int w = 0; w < kThreads / 32; ++w) v += red[w][threadIdx.x];
+    for (int w = 0; w < kWarps; ++w) v += red[w][threadIdx.x];
     part[threadIdx.x] = v;
   }
   part[kHdr + threadIdx.x] = bins;
@@ -201,22 +289,23 @@ int ctas_per_sm() {
   static int cached = 0;
   if (cached == 0) {
     int v = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, gibbs_kernel, kThreads, 0) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, gibbs_kernel<false>, kThreads, 0) !=
             cudaSuccess || v <= 0)
-      v = 4;
+      v = 2;
     cached = v;
   }
   return cached;
 }
 
-// One resident wave of CTAs; each thread runs `rounds` chains so that the
-// chains divide as evenly as possible over the wave.
+// One resident wave of CTAs; each thread runs `rounds` x kCPT chains so that
+// the chains divide as evenly as possible over the wave.
 inline void grid_shape(uint64_t n_chains, const Ctx& ctx, unsigned& grid, uint32_t& rounds) {
   const uint64_t max_ctas = (uint64_t)ctx.num_sms * ctas_per_sm();
-  const uint64_t max_threads = max_ctas * kThreads;
-  const uint64_t r = (n_chains + max_threads - 1) / max_threads;
+  const uint64_t per_round_max = max_ctas * kThreads * kCPT;
+  const uint64_t r = (n_chains + per_round_max - 1) / per_round_max;
   rounds = (uint32_t)(r ? r : 1);
-  uint64_t g = (n_chains + (uint64_t)rounds * kThreads - 1) / ((uint64_t)rounds * kThreads);
+  const uint64_t per_cta = (uint64_t)rounds * kThreads * kCPT;
+  const uint64_t g = (n_chains + per_cta - 1) / per_cta;
   grid = (unsigned)(g ? g : 1);
 }
 
@@ -235,11 +324,18 @@ cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
   GibbsArgs a;
   unsigned grid; uint32_t rounds;
   grid_shape(n_chains, ctx, grid, rounds);
-  a.n_chains = n_chains; a.n_sweeps = n_sweeps; a.burn_in = burn_in; a.base = base;
-  a.stream_id = ctx.stream_id; a.k0 = ctx.k0; a.k1 = ctx.k1; a.rounds = rounds;
+  a.n_chains = n_chains; a.base = base; a.stream_id = ctx.stream_id;
+  a.n_sweeps = (uint32_t)n_sweeps; a.burn_in = (uint32_t)burn_in; a.rounds = rounds;
+  for (int r = 0; r < 10; ++r) {
+    a.rk0[r] = ctx.k0 + (uint32_t)r * kPhiloxW0;
+    a.rk1[r] = ctx.k1 + (uint32_t)r * kPhiloxW1;
+  }
   a.x0 = x0; a.y0 = y0; a.out_x = out_x; a.out_y = out_y; a.chain_stats = chain_stats;
   a.final_xy = final_xy; a.partials = partials; a.err = ctx.err;
-  gibbs_kernel<<<grid, kThreads, 0, ctx.stream>>>(a);
+  if (out_x != nullptr || out_y != nullptr)
+    gibbs_kernel<true><<<grid, kThreads, 0, ctx.stream>>>(a);
+  else
+    gibbs_kernel<false><<<grid, kThreads, 0, ctx.stream>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || totals == nullptr) return e;
   reduce_partials_kernel<<<1, kTot, 0, ctx.stream>>>(
