@@ -38,11 +38,14 @@ UNIT = "Gsamples/s"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0          # B200_PROFILING.md fallback
 SMS, SMSP, LANES = 148, 4, 32
-# Algorithmic instruction count per Gibbs sweep:
-# Philox4x32-10 = 10 rounds x (2 IMAD.WIDE + 2 LOP3) = 40; two exact u53
-# conversions 2 x 5 = 10; x,y update 2 DADD + 2 DMUL = 4; statistics 2 DADD +
-# 3 DFMA = 5; histogram bin + ATOMS = 3; loop = 2.  Total 64 issue slots.
-GIBBS_INSTR_PER_SWEEP = 64
+# Gibbs roofline: the sweep is bound by the B200
+# FMA-heavy pipe, which runs every fp64 op (64 lanes/clk/SM) and the 32x32->64
+# IMAD.WIDE of Philox at half that rate (tools/ubench.cu, profiles/).  The
+# algorithmic work of one sweep is 17 wide multiplies (20 Philox products
+# minus the 3 that are constant along a chain) + 9 fp64 ops (2 x (1-y, mul),
+# 5 statistics) = 17*2 + 9 = 43 fp64-pipe slots; peak = 64 x 148 x f_sm.
+GIBBS_PIPE_OPS_PER_SWEEP = 43
+FP64_LANES_PER_SM = 64
 # Per Gamma sample: E[trials] x (Philox 40 + u53 5 + log 30 + sqrt
 # 12 + cospi 25 + test 10) + P(alpha<1) x (Philox 40 + u53 5 + log 30 + div 15
 # + exp 20) + load/store/queue 12 -- evaluated from the measured trial mix.
@@ -260,6 +263,7 @@ def gpu_arm(args):
     # ---- roofline of the dominant kernel + breakdown -------------------------
     sm_hz = (clk.get("sm_max_mhz") or sm_max_cfg) * 1e6
     issue_peak = SMS * SMSP * LANES * sm_hz            # thread-instructions / s
+    pipe_peak = SMS * FP64_LANES_PER_SM * sm_hz        # fp64-pipe slots / s
     # Gamma trial mix of cfg3, measured once (untimed) from the trials output
     wl.trials = torch.empty(wl.c3["n"], dtype=torch.uint8, device=wl.dev)
     B.brng_set_offset(wl.h3, wl.base3)
@@ -281,19 +285,22 @@ def gpu_arm(args):
             d.update(bound="alu", frac=round(a / issue_peak, 4), mean_trials=round(mean_trials, 5),
                      boost_frac=round(frac_boost, 4))
         elif n in ("cfg1_gibbs", "cfg5_gibbs"):
-            a = GIBBS_INSTR_PER_SWEEP * (wl.samples[n] / 2) / t
-            d.update(bound="alu", frac=round(a / issue_peak, 4),
+            a = GIBBS_PIPE_OPS_PER_SWEEP * (wl.samples[n] / 2) / t
+            d.update(bound="alu", frac=round(a / pipe_peak, 4),
                      Gsweeps_per_s=round(wl.samples[n] / 2 / t / 1e9, 3))
         bd[n] = d
     dom = max(names, key=lambda n: per[n])
     t_dom = per[dom] * 1e-3
     if dom in ("cfg1_gibbs", "cfg5_gibbs"):
-        achieved = GIBBS_INSTR_PER_SWEEP * (wl.samples[dom] / 2) / t_dom / 1e12
+        achieved = GIBBS_PIPE_OPS_PER_SWEEP * (wl.samples[dom] / 2) / t_dom / 1e12
         roof = {"kernel": "gibbs_kernel (" + dom + ")", "bound": "alu",
-                "achieved": round(achieved, 3), "peak": round(issue_peak / 1e12, 3),
-                "unit": "Tinstr/s (issue slots, 148 SM x 4 SMSP x 32 lanes x sm_max clock)",
-                "frac": round(achieved * 1e12 / issue_peak, 4),
-                "algorithmic_per_unit": f"{GIBBS_INSTR_PER_SWEEP} instr/sweep",
+                "achieved": round(achieved, 3), "peak": round(pipe_peak / 1e12, 3),
+                "unit": "T fp64-pipe ops/s (FMA-heavy pipe: 64 lanes/clk/SM x 148 SM x "
+                        "sm_max clock; IMAD.WIDE = 2 slots)",
+                "frac": round(achieved * 1e12 / pipe_peak, 4),
+                "algorithmic_per_unit": f"{GIBBS_PIPE_OPS_PER_SWEEP} pipe slots/sweep "
+                                        "(17 IMAD.WIDE x 2 + 9 fp64)",
+                "units_per_launch": wl.samples[dom] // 2,
                 "traffic": None}
     else:
         roof = {"kernel": dom, "bound": bd[dom].get("bound"), "frac": bd[dom].get("frac")}
