@@ -3,15 +3,30 @@
 // paper's BatchRNG object: engine state = (seed,
 // stream_id, block cursor); the "buffer counter" is the Philox block cursor,
 // advanced at enqueue time (R-12).
+//
+// Host buffers are streamed through the GPU in chunks with a three-stream
+// pipeline (H2D copy stream -> kernel on the handle's stream -> D2H copy
+// stream, two staging slots), so PCIe transfers in both directions overlap
+// each other and the kernels.  Chunks are cut on sample (fills: Philox-block;
+// Dirichlet: row; Gibbs: chain) boundaries and every chunk is launched at the
+// cursor / stream its first unit has in the unchunked call, so results are
+// identical to a device-pointer call.
 #include "../../include/brng.h"
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <functional>
 #include <limits>
 #include <new>
 #include <vector>
 
 #include "brng_internal.h"
+
+namespace {
+constexpr int kSlots = 2;
+constexpr size_t kChunkBytes = size_t(64) << 20;     // target staging chunk per array
+}  // namespace
 
 struct brng_handle_s {
   uint64_t seed;
@@ -23,6 +38,12 @@ struct brng_handle_s {
   unsigned long long* d_err;   // invalid-sample counter
   double* d_partials;          // Gibbs per-CTA partials
   size_t partials_cap;         // in doubles
+  // host-staging pipeline (created on the first host-pointer call)
+  cudaStream_t s_in, s_out;
+  cudaEvent_t ev_in[kSlots], ev_k[kSlots], ev_out[kSlots];
+  void* stage[kSlots];
+  size_t stage_cap;
+  bool pipe_ready;
 };
 
 namespace {
@@ -75,48 +96,125 @@ bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-// Host-buffer staging (include/brng.h "Pointers"): host inputs are copied to
-// stream-ordered device allocations, host outputs are copied back after the
-// kernel, and the call synchronises before returning.
-struct Stage {
-  cudaStream_t s;
-  struct Out { void* host; void* dev; size_t bytes; };
-  std::vector<void*> allocs;
-  std::vector<Out> outs;
-  bool any_host = false;
-  cudaError_t err = cudaSuccess;
+bool mul_ok(uint64_t a, uint64_t b) {
+  return b == 0 || a <= std::numeric_limits<uint64_t>::max() / b;
+}
 
-  explicit Stage(cudaStream_t st) : s(st) {}
-  const void* in(const void* p, size_t bytes) {
-    if (p == nullptr || bytes == 0 || is_device_ptr(p)) return p;
-    any_host = true;
-    void* d = nullptr;
-    if (err == cudaSuccess) err = cudaMallocAsync(&d, bytes, s);
-    if (err == cudaSuccess) { allocs.push_back(d); err = cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, s); }
-    return d;
-  }
-  void* out(void* p, size_t bytes) {
-    if (p == nullptr || bytes == 0 || is_device_ptr(p)) return p;
-    any_host = true;
-    void* d = nullptr;
-    if (err == cudaSuccess) err = cudaMallocAsync(&d, bytes, s);
-    if (err == cudaSuccess) { allocs.push_back(d); outs.push_back({p, d, bytes}); }
-    return d;
-  }
-  cudaError_t finish(cudaError_t launch) {
-    if (err == cudaSuccess) err = launch;
-    for (auto& o : outs)
-      if (err == cudaSuccess) err = cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDeviceToHost, s);
-    for (void* d : allocs) cudaFreeAsync(d, s);
-    if (any_host) {
-      cudaError_t e2 = cudaStreamSynchronize(s);
-      if (err == cudaSuccess) err = e2;
-    }
-    return err;
-  }
+// One array of a call.  A unit is a sample / row / chain; an array holds
+// `rows` rows of n_units * unit_bytes bytes (rows > 1: Gibbs [k][n_chains]).
+struct Arr {
+  const void* ptr;
+  size_t unit_bytes;
+  bool out;
+  size_t rows = 1;
+  bool host = false;
+  size_t slot_off = 0;        // offset of this array inside a staging slot
 };
 
-bool mul_ok(uint64_t a, uint64_t b) { return b == 0 || a <= std::numeric_limits<uint64_t>::max() / b; }
+int ensure_pipe(brng_t h, size_t slot_bytes) {
+  if (!h->pipe_ready) {
+    if (cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking) != cudaSuccess)
+      return BRNG_ERR_CUDA;
+    for (int b = 0; b < kSlots; ++b) {
+      if (cudaEventCreateWithFlags(&h->ev_in[b], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->ev_k[b], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->ev_out[b], cudaEventDisableTiming) != cudaSuccess)
+        return BRNG_ERR_CUDA;
+      h->stage[b] = nullptr;
+    }
+    h->stage_cap = 0;
+    h->pipe_ready = true;
+  }
+  if (slot_bytes > h->stage_cap) {
+    for (int b = 0; b < kSlots; ++b) {
+      if (h->stage[b]) cudaFree(h->stage[b]);
+      h->stage[b] = nullptr;
+    }
+    h->stage_cap = 0;
+    for (int b = 0; b < kSlots; ++b)
+      if (cudaMalloc(&h->stage[b], slot_bytes) != cudaSuccess) return BRNG_ERR_CUDA;
+    h->stage_cap = slot_bytes;
+  }
+  return BRNG_OK;
+}
+
+// Launch callback for units [u0, u0 + nu) with per-array device pointers.
+using Launch =
+    std::function<cudaError_t(uint64_t u0, uint64_t nu, const std::vector<void*>& dptr, bool first)>;
+
+// Run a call over n_units.  All-device arrays: one direct launch on the
+// handle's stream (asynchronous).  Any host array: chunked pipeline; returns
+// after every host output is written.
+int run(brng_t h, std::vector<Arr>& arrs, uint64_t n_units, uint64_t align, const Launch& launch) {
+  bool any_host = false;
+  for (auto& a : arrs) {
+    a.host = a.ptr != nullptr && !is_device_ptr(a.ptr);
+    any_host |= a.host;
+  }
+  if (!any_host) {
+    std::vector<void*> d;
+    for (auto& a : arrs) d.push_back(const_cast<void*>(a.ptr));
+    return cuda_status(launch(0, n_units, d, true));
+  }
+  // chunk: <= kChunkBytes of the widest host array, a multiple of align
+  size_t widest = 1;
+  for (auto& a : arrs)
+    if (a.host) widest = std::max(widest, a.unit_bytes * a.rows);
+  uint64_t chunk = std::max<uint64_t>(align, (kChunkBytes / widest) / align * align);
+  chunk = std::min<uint64_t>(chunk, n_units);
+  size_t slot = 0;
+  for (auto& a : arrs)
+    if (a.host) {
+      a.slot_off = slot;
+      slot += (a.unit_bytes * a.rows * chunk + 255) & ~size_t(255);
+    }
+  int st = ensure_pipe(h, slot);
+  if (st) return st;
+  // the first copies must not overtake earlier work of this handle's stream
+  cudaError_t e = cudaEventRecord(h->ev_k[0], h->stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(h->s_in, h->ev_k[0], 0);
+  const uint64_t n_chunks = (n_units + chunk - 1) / chunk;
+  for (uint64_t j = 0; j < n_chunks && e == cudaSuccess; ++j) {
+    const int b = (int)(j % kSlots);
+    const uint64_t u0 = j * chunk, nu = std::min(chunk, n_units - u0);
+    char* base = static_cast<char*>(h->stage[b]);
+    if (j >= kSlots) e = cudaStreamWaitEvent(h->s_in, h->ev_out[b], 0);   // slot free again
+    std::vector<void*> d;
+    for (auto& a : arrs) {
+      if (!a.host) {
+        d.push_back(a.ptr ? static_cast<char*>(const_cast<void*>(a.ptr)) + u0 * a.unit_bytes
+                          : nullptr);
+        continue;
+      }
+      char* dp = base + a.slot_off;
+      d.push_back(dp);
+      if (!a.out && e == cudaSuccess) {
+        const char* hp = static_cast<const char*>(a.ptr) + u0 * a.unit_bytes;
+        e = cudaMemcpy2DAsync(dp, nu * a.unit_bytes, hp, n_units * a.unit_bytes,
+                              nu * a.unit_bytes, a.rows, cudaMemcpyHostToDevice, h->s_in);
+      }
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_in[b], h->s_in);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, h->ev_in[b], 0);
+    if (e == cudaSuccess) e = launch(u0, nu, d, j == 0);
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_k[b], h->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->s_out, h->ev_k[b], 0);
+    for (size_t k = 0; k < arrs.size() && e == cudaSuccess; ++k) {
+      const Arr& a = arrs[k];
+      if (!a.host || !a.out) continue;
+      char* hp = static_cast<char*>(const_cast<void*>(a.ptr)) + u0 * a.unit_bytes;
+      e = cudaMemcpy2DAsync(hp, n_units * a.unit_bytes, d[k], nu * a.unit_bytes,
+                            nu * a.unit_bytes, a.rows, cudaMemcpyDeviceToHost, h->s_out);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_out[b], h->s_out);
+  }
+  cudaError_t e2 = cudaStreamSynchronize(h->s_out);
+  cudaError_t e3 = cudaStreamSynchronize(h->stream);
+  if (e == cudaSuccess) e = e2;
+  if (e == cudaSuccess) e = e3;
+  return cuda_status(e);
+}
 
 int fill_common(brng_t h, int dist, int dtype, const void* p0, const void* p1, void* out,
                 uint64_t n, size_t esize) {
@@ -130,16 +228,12 @@ int fill_common(brng_t h, int dist, int dtype, const void* p0, const void* p1, v
   const uint64_t per = (dtype == brng::kF64) ? 2 : 4;
   uint64_t base;
   if ((st = reserve(h, n, per, 1, &base))) return st;
-  Stage sg(h->stream);
-  const size_t bytes = (size_t)n * esize;
-  const void* d0 = sg.in(p0, p0 ? bytes : 0);
-  const void* d1 = sg.in(p1, p1 ? bytes : 0);
-  void* dout = sg.out(out, bytes);
-  cudaError_t e = sg.err == cudaSuccess
-                      ? brng::launch_fill(dist, dtype, d0, d1, dout, n, base, make_ctx(h))
-                      : sg.err;
-  e = sg.finish(e);
-  if (e != cudaSuccess) return BRNG_ERR_CUDA;
+  std::vector<Arr> arrs = {{p0, esize, false}, {p1, esize, false}, {out, esize, true}};
+  const Ctx ctx = make_ctx(h);
+  st = run(h, arrs, n, per, [&](uint64_t u0, uint64_t nu, const std::vector<void*>& d, bool) {
+    return brng::launch_fill(dist, dtype, d[0], d[1], d[2], nu, base + u0 / per, ctx);
+  });
+  if (st) return st;
   commit(h, n, per, 1);
   return BRNG_OK;
 }
@@ -153,17 +247,14 @@ int gamma_common(brng_t h, int dtype, const void* alpha, const void* beta, void*
   if (st) return st;
   uint64_t base;
   if ((st = reserve(h, n, 1, BRNG_GAMMA_STRIDE, &base))) return st;
-  Stage sg(h->stream);
-  const size_t bytes = (size_t)n * esize;
-  const void* da = sg.in(alpha, bytes);
-  const void* db = sg.in(beta, bytes);
-  void* dout = sg.out(out, bytes);
-  uint8_t* dtr = static_cast<uint8_t*>(sg.out(trials, trials ? (size_t)n : 0));
-  cudaError_t e = sg.err == cudaSuccess
-                      ? brng::launch_gamma(dtype, da, db, dout, dtr, n, base, make_ctx(h))
-                      : sg.err;
-  e = sg.finish(e);
-  if (e != cudaSuccess) return BRNG_ERR_CUDA;
+  std::vector<Arr> arrs = {{alpha, esize, false}, {beta, esize, false}, {out, esize, true},
+                           {trials, 1, true}};
+  const Ctx ctx = make_ctx(h);
+  st = run(h, arrs, n, 1, [&](uint64_t u0, uint64_t nu, const std::vector<void*>& d, bool) {
+    return brng::launch_gamma(dtype, d[0], d[1], d[2], static_cast<uint8_t*>(d[3]), nu,
+                              base + (uint64_t)BRNG_GAMMA_STRIDE * u0, ctx);
+  });
+  if (st) return st;
   commit(h, n, 1, BRNG_GAMMA_STRIDE);
   return BRNG_OK;
 }
@@ -180,16 +271,13 @@ int dirichlet_common(brng_t h, int dtype, const void* alpha, uint64_t n_rows, ui
   if (st) return st;
   uint64_t base;
   if ((st = reserve(h, n, 1, BRNG_GAMMA_STRIDE, &base))) return st;
-  Stage sg(h->stream);
-  const size_t bytes = (size_t)n * esize;
-  const void* da = sg.in(alpha, bytes);
-  void* dout = sg.out(out, bytes);
-  uint8_t* dtr = static_cast<uint8_t*>(sg.out(trials, trials ? (size_t)n : 0));
-  cudaError_t e = sg.err == cudaSuccess
-                      ? brng::launch_dirichlet(dtype, da, n_rows, k, dout, dtr, base, make_ctx(h))
-                      : sg.err;
-  e = sg.finish(e);
-  if (e != cudaSuccess) return BRNG_ERR_CUDA;
+  std::vector<Arr> arrs = {{alpha, esize * k, false}, {out, esize * k, true}, {trials, k, true}};
+  const Ctx ctx = make_ctx(h);
+  st = run(h, arrs, n_rows, 1, [&](uint64_t r0, uint64_t nr, const std::vector<void*>& d, bool) {
+    return brng::launch_dirichlet(dtype, d[0], nr, k, d[1], static_cast<uint8_t*>(d[2]),
+                                  base + (uint64_t)BRNG_GAMMA_STRIDE * r0 * k, ctx);
+  });
+  if (st) return st;
   commit(h, n, 1, BRNG_GAMMA_STRIDE);
   return BRNG_OK;
 }
@@ -225,6 +313,7 @@ int brng_create(uint64_t seed, uint64_t stream_id, brng_t* out) {
   h->seed = seed; h->stream_id = stream_id; h->cursor = 0;
   h->device = dev; h->num_sms = sms; h->stream = nullptr;
   h->d_partials = nullptr; h->partials_cap = 0;
+  h->pipe_ready = false; h->stage_cap = 0;
   if (cudaMalloc(&h->d_err, sizeof(unsigned long long)) != cudaSuccess ||
       cudaMemset(h->d_err, 0, sizeof(unsigned long long)) != cudaSuccess) {
     delete h;
@@ -240,6 +329,18 @@ int brng_destroy(brng_t h) {
   cudaStreamSynchronize(h->stream);
   cudaFree(h->d_err);
   if (h->d_partials) cudaFree(h->d_partials);
+  if (h->pipe_ready) {
+    cudaStreamSynchronize(h->s_in);
+    cudaStreamSynchronize(h->s_out);
+    for (int b = 0; b < kSlots; ++b) {
+      if (h->stage[b]) cudaFree(h->stage[b]);
+      cudaEventDestroy(h->ev_in[b]);
+      cudaEventDestroy(h->ev_k[b]);
+      cudaEventDestroy(h->ev_out[b]);
+    }
+    cudaStreamDestroy(h->s_in);
+    cudaStreamDestroy(h->s_out);
+  }
   delete h;
   return BRNG_OK;
 }
@@ -261,7 +362,8 @@ int brng_set_offset(brng_t h, uint64_t c) {
 }
 int brng_get_key(brng_t h, uint64_t* seed, uint64_t* stream_id) {
   if (!h || !seed || !stream_id) return BRNG_ERR_NULL;
-  *seed = h->seed; *stream_id = h->stream_id;
+  *seed = h->seed;
+  *stream_id = h->stream_id;
   return BRNG_OK;
 }
 int brng_synchronize(brng_t h) {
@@ -340,32 +442,49 @@ int brng_gibbs_triangle(brng_t h, uint64_t n_chains, uint64_t n_sweeps, const do
   if (st) return st;
   uint64_t base;
   if ((st = reserve(h, n_sweeps, 1, 1, &base))) return st;
-  Ctx ctx = make_ctx(h);
+  const Ctx ctx = make_ctx(h);
   const size_t need = brng::gibbs_partials_len(n_chains, ctx);
   if (need > h->partials_cap) {
     if (h->d_partials) {
       cudaStreamSynchronize(h->stream);
       cudaFree(h->d_partials);
-      h->d_partials = nullptr; h->partials_cap = 0;
+      h->d_partials = nullptr;
+      h->partials_cap = 0;
     }
     if (cudaMalloc(&h->d_partials, need * sizeof(double)) != cudaSuccess) return BRNG_ERR_CUDA;
     h->partials_cap = need;
   }
-  Stage sg(h->stream);
-  const size_t nc8 = (size_t)n_chains * 8;
-  const double* dx0 = static_cast<const double*>(sg.in(x0, x0 ? nc8 : 0));
-  const double* dy0 = static_cast<const double*>(sg.in(y0, y0 ? nc8 : 0));
-  double* dox = static_cast<double*>(sg.out(out_x, out_x ? nc8 * n_sweeps : 0));
-  double* doy = static_cast<double*>(sg.out(out_y, out_y ? nc8 * n_sweeps : 0));
-  double* dst = static_cast<double*>(sg.out(chain_stats, chain_stats ? nc8 * 5 : 0));
-  double* dfx = static_cast<double*>(sg.out(final_xy, final_xy ? nc8 * 2 : 0));
-  double* dtot = static_cast<double*>(sg.out(totals, totals ? BRNG_TOTALS_LEN * 8 : 0));
-  cudaError_t e = sg.err == cudaSuccess
-                      ? brng::launch_gibbs(n_chains, n_sweeps, dx0, dy0, burn_in, dox, doy, dst,
-                                           dfx, dtot, h->d_partials, base, ctx)
-                      : sg.err;
-  e = sg.finish(e);
-  if (e != cudaSuccess) return BRNG_ERR_CUDA;
+  // totals belongs to the call, not to a chain: a host totals pointer gets a
+  // device scratch that every chunk accumulates into
+  double* dtot = totals;
+  const bool host_tot = totals != nullptr && !is_device_ptr(totals);
+  if (host_tot && cudaMallocAsync(reinterpret_cast<void**>(&dtot), BRNG_TOTALS_LEN * 8,
+                                  h->stream) != cudaSuccess)
+    return BRNG_ERR_CUDA;
+  std::vector<Arr> arrs = {{x0, 8, false},
+                           {y0, 8, false},
+                           {out_x, 8, true, (size_t)n_sweeps},
+                           {out_y, 8, true, (size_t)n_sweeps},
+                           {chain_stats, 8, true, 5},
+                           {final_xy, 8, true, 2}};
+  st = run(h, arrs, n_chains, 1,
+           [&](uint64_t c0, uint64_t nc, const std::vector<void*>& d, bool first) {
+             Ctx cc = ctx;
+             cc.stream_id = ctx.stream_id + c0;
+             return brng::launch_gibbs(nc, n_sweeps, static_cast<const double*>(d[0]),
+                                       static_cast<const double*>(d[1]), burn_in,
+                                       static_cast<double*>(d[2]), static_cast<double*>(d[3]),
+                                       static_cast<double*>(d[4]), static_cast<double*>(d[5]),
+                                       dtot, h->d_partials, base, cc, !first);
+           });
+  if (host_tot) {
+    cudaError_t e = cudaMemcpyAsync(totals, dtot, BRNG_TOTALS_LEN * 8, cudaMemcpyDeviceToHost,
+                                    h->stream);
+    cudaFreeAsync(dtot, h->stream);
+    cudaError_t e2 = cudaStreamSynchronize(h->stream);
+    if (!st && (e != cudaSuccess || e2 != cudaSuccess)) st = BRNG_ERR_CUDA;
+  }
+  if (st) return st;
   commit(h, n_sweeps, 1, 1);
   return BRNG_OK;
 }

@@ -32,6 +32,7 @@ size_t gibbs_partials_len(uint64_t n_chains, const Ctx& ctx);
 cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
                          const double* y0, uint64_t burn_in, double* out_x, double* out_y,
                          double* chain_stats, double* final_xy, double* totals,
-                         double* partials, uint64_t base, const Ctx& ctx);
+                         double* partials, uint64_t base, const Ctx& ctx,
+                         bool accumulate_totals = false);
 
 }  // namespace brng

@@ -273,16 +273,18 @@ __global__ void __launch_bounds__(kThreads, BRNG_GIBBS_MINB) gibbs_kernel(GibbsA
 }
 
 // K7: totals[j] = sum over CTAs of partials[cta][j], CTA order fixed.
+// accumulate != 0: add to totals (a host-staged call processed in chunks).
 __global__ void __launch_bounds__(kTot) reduce_partials_kernel(const double* partials,
                                                               uint32_t n_parts, double* totals,
-                                                              double n_chains, double n_samples) {
+                                                              double n_chains, double n_samples,
+                                                              int accumulate) {
   const uint32_t j = threadIdx.x;
   double v = 0.0;
   if (j < 8 || j >= kHdr)
     for (uint32_t p = 0; p < n_parts; ++p) v += partials[(uint64_t)p * kTot + j];
   if (j == 8) v = n_chains;
   if (j == 9) v = n_samples;
-  totals[j] = v;
+  totals[j] = accumulate ? totals[j] + v : v;
 }
 
 int ctas_per_sm() {
@@ -311,16 +313,16 @@ inline void grid_shape(uint64_t n_chains, const Ctx& ctx, unsigned& grid, uint32
 
 }  // namespace
 
-size_t gibbs_partials_len(uint64_t n_chains, const Ctx& ctx) {
-  unsigned g; uint32_t r;
-  grid_shape(n_chains, ctx, g, r);
-  return (size_t)g * kTot;
+// Enough for any launch shape (one resident wave), so chunked calls that
+// launch different grids can share the handle's scratch.
+size_t gibbs_partials_len(uint64_t /*n_chains*/, const Ctx& ctx) {
+  return (size_t)ctx.num_sms * ctas_per_sm() * kTot;
 }
 
 cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
                          const double* y0, uint64_t burn_in, double* out_x, double* out_y,
                          double* chain_stats, double* final_xy, double* totals,
-                         double* partials, uint64_t base, const Ctx& ctx) {
+                         double* partials, uint64_t base, const Ctx& ctx, bool accumulate) {
   GibbsArgs a;
   unsigned grid; uint32_t rounds;
   grid_shape(n_chains, ctx, grid, rounds);
@@ -339,7 +341,8 @@ cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || totals == nullptr) return e;
   reduce_partials_kernel<<<1, kTot, 0, ctx.stream>>>(
-      partials, grid, totals, (double)n_chains, (double)n_chains * (double)(n_sweeps - burn_in));
+      partials, grid, totals, (double)n_chains, (double)n_chains * (double)(n_sweeps - burn_in),
+      accumulate ? 1 : 0);
   return cudaGetLastError();
 }
 

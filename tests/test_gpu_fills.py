@@ -185,3 +185,24 @@ def test_cfg2_full_size_sampled():
     x = out_u[idx].cpu().numpy()
     assert np.all(x >= a) and np.all(x <= b)
     assert_ks_uniform(pit_uniform(x, a, b), "cfg2 uniform PIT")
+
+
+def test_host_pipeline_multi_chunk_equals_device():
+    # > 64 MB per array: the host path runs as several pipelined chunks
+    n = 40_000_003
+    p = workloads.cfg2_params(n, seed=12)
+    mu, sg = p["mu"].numpy(), p["sigma"].numpy()
+    out_h = np.empty(n, np.float32)
+    with handle(12, 0, 5) as h:
+        B.brng_gaussian_f32(h, mu, sg, out_h, n)
+        c_after = B.brng_get_offset(h)
+    with handle(12, 0, 5) as h:
+        out_d = torch.empty(n, device=dev())
+        B.brng_gaussian_f32(h, p["mu"].to(dev()), p["sigma"].to(dev()), out_d, n)
+        assert B.brng_get_offset(h) == c_after
+    assert np.array_equal(out_h, out_d.cpu().numpy())
+    # mixed: device inputs, host output
+    with handle(12, 0, 5) as h:
+        out_m = np.empty(n, np.float32)
+        B.brng_gaussian_f32(h, p["mu"].to(dev()), p["sigma"].to(dev()), out_m, n)
+    assert np.array_equal(out_m, out_h)

@@ -182,3 +182,25 @@ def test_cfg4_full_size_sampled():
     a = alpha[rows].double().cpu().numpy()
     A = a.sum(axis=1, keepdims=True)
     assert_ks_uniform(pit_beta(x, a, A - a).reshape(-1), "cfg4 Beta-marginal PIT")
+
+
+def test_host_pipeline_multi_chunk_gamma_dirichlet():
+    n = 10_000_001                                    # 80 MB per f64 array -> 2 chunks
+    p = workloads.cfg3_params(n, seed=21)
+    oh = np.empty(n); th = np.empty(n, np.uint8)
+    with handle(21) as h:
+        B.brng_gamma_f64(h, p["alpha"].numpy(), p["beta"].numpy(), oh, n, th)
+    with handle(21) as h:
+        od = torch.empty(n, dtype=torch.float64, device=dev())
+        td = torch.empty(n, dtype=torch.uint8, device=dev())
+        B.brng_gamma_f64(h, p["alpha"].to(dev()), p["beta"].to(dev()), od, n, td)
+    assert np.array_equal(oh, od.cpu().numpy()) and np.array_equal(th, td.cpu().numpy())
+    D, K = 100_003, 256                               # 102 MB f32 -> 2 chunks
+    al = workloads.cfg4_params(D, K, seed=22)
+    xh = np.empty((D, K), np.float32)
+    with handle(22) as h:
+        B.brng_dirichlet_f32(h, al.numpy(), D, K, xh, None)
+    with handle(22) as h:
+        xd = torch.empty(D, K, device=dev())
+        B.brng_dirichlet_f32(h, al.to(dev()), D, K, xd, None)
+    assert np.array_equal(xh, xd.cpu().numpy())

@@ -142,3 +142,15 @@ def test_cfg5_full_size():
     from tests.stats_util import assert_ks_uniform
     fxv = g["final_xy"][0]
     assert_ks_uniform(2 * fxv - fxv * fxv, "cfg5 final-x marginal")
+
+
+def test_host_pipeline_multi_chunk_gibbs():
+    nc, ns = 3_000_017, 16                            # chain_stats 120 MB -> 2 chunks
+    g = _run(42, 0, 0, nc, ns, samples=False)
+    st = np.empty((5, nc)); fx = np.empty((2, nc)); tot = np.empty(B.TOTALS_LEN)
+    with handle(42) as h:
+        B.brng_gibbs_triangle(h, nc, ns, None, None, 0, None, None, st, fx, tot)
+        assert B.brng_get_offset(h) == ns
+    assert np.array_equal(st, g["chain_stats"]) and np.array_equal(fx, g["final_xy"])
+    assert np.array_equal(tot[HDR:], g["totals"][HDR:])
+    np.testing.assert_allclose(tot[:HDR], g["totals"][:HDR], rtol=1e-12)
