@@ -113,7 +113,29 @@ __device__ __forceinline__ ChainKey chain_key(uint64_t stream, uint32_t pos_hi,
   return ck;
 }
 
-__device__ __forceinline__ uint4 chain_block(const ChainKey& ck, uint64_t p0, const GibbsArgs& a) {
+// Round keys of rounds 2..9.  With BRNG_GIBBS_KEYREG they are pinned in
+// registers (an opaque asm barrier stops ptxas from re-loading them from the
+// constant bank every sweep).
+#ifndef BRNG_GIBBS_KEYREG
+#define BRNG_GIBBS_KEYREG 1
+#endif
+struct RoundKeys {
+  uint32_t k0[8], k1[8];
+};
+__device__ __forceinline__ RoundKeys load_keys(const GibbsArgs& a) {
+  RoundKeys rk;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    rk.k0[r] = a.rk0[r + 2];
+    rk.k1[r] = a.rk1[r + 2];
+#if BRNG_GIBBS_KEYREG
+    asm volatile("" : "+r"(rk.k0[r]), "+r"(rk.k1[r]));
+#endif
+  }
+  return rk;
+}
+
+__device__ __forceinline__ uint4 chain_block(const ChainKey& ck, uint64_t p0, const RoundKeys& rk) {
   // rounds 1 and 2 (round 1 is free: its products are chain constants or p0)
   const uint32_t z1 = (uint32_t)(p0 >> 32) ^ ck.c3k1;
   const uint64_t p1 = (uint64_t)kPhiloxM1 * z1;
@@ -123,7 +145,7 @@ __device__ __forceinline__ uint4 chain_block(const ChainKey& ck, uint64_t p0, co
   c.z = (uint32_t)p0 ^ ck.a2;
   c.w = ck.b2;
 #pragma unroll
-  for (int r = 2; r < 10; ++r) c = philox_round(c, a.rk0[r], a.rk1[r]);
+  for (int r = 0; r < 8; ++r) c = philox_round(c, rk.k0[r], rk.k1[r]);
   return c;
 }
 
@@ -136,26 +158,26 @@ struct Chain {
 };
 
 // Sweeps [s_begin, s_end) of the thread's kCPT chains.
-template <bool STORE, bool STATS>
-__device__ __forceinline__ void sweeps(const GibbsArgs& a, uint32_t s_begin, uint32_t s_end,
-                                       Chain (&ch)[kCPT], uint32_t hist_base) {
+template <bool STORE, bool STATS, int CPT>
+__device__ __forceinline__ void sweeps(const GibbsArgs& a, const RoundKeys& rk, uint32_t s_begin,
+                                       uint32_t s_end, Chain (&ch)[CPT], uint32_t hist_base) {
   uint32_t s = s_begin;
   while (s < s_end) {
     const uint64_t pos = a.base + s;
     const uint32_t pos_lo = (uint32_t)pos;
     const uint64_t room = 0x100000000ull - pos_lo;     // sweeps before lo(pos) wraps
     const uint32_t e = ((uint64_t)(s_end - s) < room) ? s_end : (uint32_t)(s + room);
-    ChainKey ck[kCPT];
+    ChainKey ck[CPT];
 #pragma unroll
-    for (int k = 0; k < kCPT; ++k)
+    for (int k = 0; k < CPT; ++k)
       ck[k] = chain_key(a.stream_id + ch[k].c, (uint32_t)(pos >> 32), a);
     uint64_t p0 = (uint64_t)kPhiloxM0 * pos_lo;
 #pragma unroll kUnroll
     for (; s < e; ++s) {
 #pragma unroll
-      for (int k = 0; k < kCPT; ++k) {
+      for (int k = 0; k < CPT; ++k) {
         Chain& q = ch[k];
-        const uint4 w = chain_block(ck[k], p0, a);
+        const uint4 w = chain_block(ck[k], p0, rk);
         // x = fl(fl(1-y) u53)  <=>  X = fl(fl(1-y) m),  1-y = fma(Y, -2^-53, 1)
         q.X = __dmul_rn(__fma_rn(q.Y, -kTwoM53, 1.0), m53(w.x, w.y));
         q.Y = __dmul_rn(__fma_rn(q.X, -kTwoM53, 1.0), m53(w.z, w.w));
@@ -182,29 +204,38 @@ __device__ __forceinline__ double warp_sum(double s) {
   return s;
 }
 
-template <bool STORE>
-__global__ void __launch_bounds__(kThreads, BRNG_GIBBS_MINB) gibbs_kernel(GibbsArgs a) {
+// THREADS threads x CPT chains per thread.  The bulk configuration is
+// <.., kCPT, kThreads> (two chains per thread for ILP); small chain counts
+// (cfg1: 1024 chains) use one chain per thread in 64-thread CTAs to spread
+// the latency-bound chains over more SMs.
+template <bool STORE, int CPT, int THREADS>
+__global__ void __launch_bounds__(THREADS, (THREADS == kThreads ? BRNG_GIBBS_MINB : 1))
+gibbs_kernel(GibbsArgs a) {
+  constexpr int kW = THREADS / 32;
+  constexpr int kBinsPerThread = 256 / THREADS;
   __shared__ uint32_t hist[257];              // [256] = sink for dead chains
-  __shared__ double red[kWarps][8];
+  __shared__ double red[kW][8];
   const uint32_t hist_base = (uint32_t)__cvta_generic_to_shared(hist);
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  hist[threadIdx.x] = 0;                       // kThreads == 256 bins
+  for (int b = threadIdx.x; b < 257; b += THREADS) hist[b] = 0;
   if (lane < 8) red[wid][lane] = 0.0;
-  double bins = 0.0;                           // this thread's bin, accumulated
+  double bins[kBinsPerThread];                 // bins threadIdx.x + j*THREADS, accumulated
+#pragma unroll
+  for (int j = 0; j < kBinsPerThread; ++j) bins[j] = 0.0;
   uint32_t nbad = 0;
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
   const double n = (double)(a.n_sweeps - a.burn_in);
   const double nm1 = __dsub_rn(n, 1.0);
+  const RoundKeys rk = load_keys(a);
   __syncthreads();
 
-  const uint64_t per_round = (uint64_t)gridDim.x * kThreads * kCPT;
+  const uint64_t per_round = (uint64_t)gridDim.x * THREADS * CPT;
   for (uint32_t rnd = 0; rnd < a.rounds; ++rnd) {
-    Chain ch[kCPT];
+    Chain ch[CPT];
 #pragma unroll
-    for (int k = 0; k < kCPT; ++k) {
+    for (int k = 0; k < CPT; ++k) {
       Chain& q = ch[k];
-      q.c = (uint64_t)rnd * per_round + ((uint64_t)blockIdx.x * kCPT + k) * kThreads +
-            threadIdx.x;
+      q.c = (uint64_t)rnd * per_round + ((uint64_t)blockIdx.x * CPT + k) * THREADS + threadIdx.x;
       const bool real = q.c < a.n_chains;
       const double x = (real && a.x0) ? a.x0[q.c] : 0.5;
       const double y = (real && a.y0) ? a.y0[q.c] : 0.5;
@@ -215,12 +246,12 @@ __global__ void __launch_bounds__(kThreads, BRNG_GIBBS_MINB) gibbs_kernel(GibbsA
       q.Y = __dmul_rn(valid ? y : qnan, kTwo53);
       q.S1X = q.S2X = q.S1Y = q.S2Y = q.SXY = 0.0;
     }
-    sweeps<STORE, false>(a, 0, a.burn_in, ch, hist_base);
-    sweeps<STORE, true>(a, a.burn_in, a.n_sweeps, ch, hist_base);
+    sweeps<STORE, false, CPT>(a, rk, 0, a.burn_in, ch, hist_base);
+    sweeps<STORE, true, CPT>(a, rk, a.burn_in, a.n_sweeps, ch, hist_base);
 
     double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-    for (int k = 0; k < kCPT; ++k) {
+    for (int k = 0; k < CPT; ++k) {
       const Chain& q = ch[k];
       if (q.c >= a.n_chains) continue;
       const double s1x = __dmul_rn(q.S1X, kTwoM53), s1y = __dmul_rn(q.S1Y, kTwoM53);
@@ -257,18 +288,22 @@ __global__ void __launch_bounds__(kThreads, BRNG_GIBBS_MINB) gibbs_kernel(GibbsA
     }
     // drain the u32 shared histogram every round (< 512 * 2^23 = 2^32 counts)
     __syncthreads();
-    bins += (double)hist[threadIdx.x];
-    hist[threadIdx.x] = 0;
+#pragma unroll
+    for (int j = 0; j < kBinsPerThread; ++j) {
+      bins[j] += (double)hist[threadIdx.x + j * THREADS];
+      hist[threadIdx.x + j * THREADS] = 0;
+    }
     __syncthreads();
   }
 
   double* part = a.partials + (uint64_t)blockIdx.x * kTot;
   if (threadIdx.x < 8) {
     double v = 0.0;
-    for (int w = 0; w < kWarps; ++w) v += red[w][threadIdx.x];
+    for (int w = 0; w < kW; ++w) v += red[w][threadIdx.x];
     part[threadIdx.x] = v;
   }
-  part[kHdr + threadIdx.x] = bins;
+#pragma unroll
+  for (int j = 0; j < kBinsPerThread; ++j) part[kHdr + threadIdx.x + j * THREADS] = bins[j];
   flush_errors(a.err, nbad);
 }
 
@@ -287,28 +322,48 @@ __global__ void __launch_bounds__(kTot) reduce_partials_kernel(const double* par
   totals[j] = accumulate ? totals[j] + v : v;
 }
 
-int ctas_per_sm() {
-  static int cached = 0;
-  if (cached == 0) {
-    int v = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, gibbs_kernel<false>, kThreads, 0) !=
-            cudaSuccess || v <= 0)
-      v = 2;
-    cached = v;
-  }
+constexpr int kSmallThreads = 64;
+constexpr int kSmallCPT = 1;
+
+template <typename K>
+int occupancy(K kernel, int threads) {
+  int v = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, threads, 0) != cudaSuccess ||
+      v <= 0)
+    v = 1;
+  return v;
+}
+int ctas_per_sm_bulk() {
+  static int cached = occupancy(gibbs_kernel<false, kCPT, kThreads>, kThreads);
+  return cached;
+}
+int ctas_per_sm_small() {
+  static int cached = occupancy(gibbs_kernel<true, kSmallCPT, kSmallThreads>, kSmallThreads);
   return cached;
 }
 
-// One resident wave of CTAs; each thread runs `rounds` x kCPT chains so that
-// the chains divide as evenly as possible over the wave.
-inline void grid_shape(uint64_t n_chains, const Ctx& ctx, unsigned& grid, uint32_t& rounds) {
-  const uint64_t max_ctas = (uint64_t)ctx.num_sms * ctas_per_sm();
-  const uint64_t per_round_max = max_ctas * kThreads * kCPT;
+// Launch shape: `threads` x `cpt` chains per CTA per round, one resident wave
+// of CTAs; each thread runs `rounds` rounds so chains divide evenly.
+struct Shape {
+  unsigned grid;
+  uint32_t rounds;
+  bool small;
+};
+inline Shape grid_shape(uint64_t n_chains, const Ctx& ctx) {
+  Shape sh;
+  const uint64_t bulk_wave = (uint64_t)ctx.num_sms * ctas_per_sm_bulk() * kThreads * kCPT;
+  sh.small = n_chains < bulk_wave / 2;
+  const int threads = sh.small ? kSmallThreads : kThreads;
+  const int cpt = sh.small ? kSmallCPT : kCPT;
+  const uint64_t max_ctas =
+      (uint64_t)ctx.num_sms * (sh.small ? ctas_per_sm_small() : ctas_per_sm_bulk());
+  const uint64_t per_round_max = max_ctas * threads * cpt;
   const uint64_t r = (n_chains + per_round_max - 1) / per_round_max;
-  rounds = (uint32_t)(r ? r : 1);
-  const uint64_t per_cta = (uint64_t)rounds * kThreads * kCPT;
+  sh.rounds = (uint32_t)(r ? r : 1);
+  const uint64_t per_cta = (uint64_t)sh.rounds * threads * cpt;
   const uint64_t g = (n_chains + per_cta - 1) / per_cta;
-  grid = (unsigned)(g ? g : 1);
+  sh.grid = (unsigned)(g ? g : 1);
+  return sh;
 }
 
 }  // namespace
@@ -316,7 +371,8 @@ inline void grid_shape(uint64_t n_chains, const Ctx& ctx, unsigned& grid, uint32
 // Enough for any launch shape (one resident wave), so chunked calls that
 // launch different grids can share the handle's scratch.
 size_t gibbs_partials_len(uint64_t /*n_chains*/, const Ctx& ctx) {
-  return (size_t)ctx.num_sms * ctas_per_sm() * kTot;
+  const int c = ctas_per_sm_bulk() > ctas_per_sm_small() ? ctas_per_sm_bulk() : ctas_per_sm_small();
+  return (size_t)ctx.num_sms * c * kTot;
 }
 
 cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
@@ -324,8 +380,9 @@ cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
                          double* chain_stats, double* final_xy, double* totals,
                          double* partials, uint64_t base, const Ctx& ctx, bool accumulate) {
   GibbsArgs a;
-  unsigned grid; uint32_t rounds;
-  grid_shape(n_chains, ctx, grid, rounds);
+  const Shape sh = grid_shape(n_chains, ctx);
+  const unsigned grid = sh.grid;
+  const uint32_t rounds = sh.rounds;
   a.n_chains = n_chains; a.base = base; a.stream_id = ctx.stream_id;
   a.n_sweeps = (uint32_t)n_sweeps; a.burn_in = (uint32_t)burn_in; a.rounds = rounds;
   for (int r = 0; r < 10; ++r) {
@@ -334,10 +391,18 @@ cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
   }
   a.x0 = x0; a.y0 = y0; a.out_x = out_x; a.out_y = out_y; a.chain_stats = chain_stats;
   a.final_xy = final_xy; a.partials = partials; a.err = ctx.err;
-  if (out_x != nullptr || out_y != nullptr)
-    gibbs_kernel<true><<<grid, kThreads, 0, ctx.stream>>>(a);
-  else
-    gibbs_kernel<false><<<grid, kThreads, 0, ctx.stream>>>(a);
+  const bool store = out_x != nullptr || out_y != nullptr;
+  if (sh.small) {
+    if (store)
+      gibbs_kernel<true, kSmallCPT, kSmallThreads><<<grid, kSmallThreads, 0, ctx.stream>>>(a);
+    else
+      gibbs_kernel<false, kSmallCPT, kSmallThreads><<<grid, kSmallThreads, 0, ctx.stream>>>(a);
+  } else {
+    if (store)
+      gibbs_kernel<true, kCPT, kThreads><<<grid, kThreads, 0, ctx.stream>>>(a);
+    else
+      gibbs_kernel<false, kCPT, kThreads><<<grid, kThreads, 0, ctx.stream>>>(a);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || totals == nullptr) return e;
   reduce_partials_kernel<<<1, kTot, 0, ctx.stream>>>(
