@@ -54,6 +54,22 @@ GAMMA_BOOST_INSTR = 110
 GAMMA_SAMPLE_INSTR = 12
 
 
+def ncu_traffic(kernel_substr):
+    """DRAM bytes (read + write) per launch of a kernel from the committed ncu
+    --set full summary (profiles/*_ncu.json, tools/ncu_summary.py), or None."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu.json"))):
+        try:
+            with open(path) as f:
+                for k in json.load(f)["kernels"]:
+                    if kernel_substr in k.get("kernel", "") and "traffic_GB" in k:
+                        best = (k["traffic_GB"] * 1e9, os.path.basename(path))
+        except Exception:
+            continue
+    return best
+
+
 def load_peaks():
     try:
         with open(PEAKS_PATH) as f:
@@ -302,6 +318,11 @@ def gpu_arm(args):
                                         "(17 IMAD.WIDE x 2 + 9 fp64)",
                 "units_per_launch": wl.samples[dom] // 2,
                 "traffic": None}
+        tr = ncu_traffic("gibbs_kernel<0, 2, 256>")
+        if tr is not None:
+            roof["traffic"] = int(tr[0])
+            roof["traffic_source"] = tr[1] + " (ncu --set full, dram__bytes_read+write per "\
+                "launch; algorithmic = chain_stats + final_xy writes 0.94 GB)"
     else:
         roof = {"kernel": dom, "bound": bd[dom].get("bound"), "frac": bd[dom].get("frac")}
     roof["peak_source"] = peak_kind
