@@ -69,6 +69,12 @@ def lib():
                 for nm in ("orc_uniform_", "orc_gaussian_", "orc_exponential_", "orc_gamma_",
                            "orc_dirichlet_"):
                     getattr(L, nm + sfx).restype = u64
+            for sfx in ("f32", "f64"):
+                getattr(L, "orc_log_uniform_" + sfx).argtypes = [u64, u64, u64, vp, u64, u64]
+                getattr(L, "orc_laplace_" + sfx).argtypes = [u64, u64, u64, vp, vp, vp, u64, u64]
+                getattr(L, "orc_weibull_" + sfx).argtypes = [u64, u64, u64, vp, vp, vp, u64, u64]
+                getattr(L, "orc_laplace_" + sfx).restype = u64
+                getattr(L, "orc_weibull_" + sfx).restype = u64
             L.orc_mt_trial.argtypes = [dbl, dbl, dbl, dbl, dbl, vp, vp, vp]
             L.orc_mt_trial.restype = i32
             L.orc_mt_consts.argtypes = [dbl, vp, vp]
@@ -173,6 +179,31 @@ def exponential(seed, stream, base, lam, i0=0, dtype=None):
     lam = _c(lam, dtype); out = np.empty(lam.shape, dtype)
     nbad = getattr(lib(), "orc_exponential_" + _sfx(dtype))(seed, stream, base, _p(lam),
                                                              _p(out), i0, lam.size)
+    return out, int(nbad)
+
+
+# --------------------------------------------------------------------------
+# 3b. NEXT row N2: log-uniform, Laplace, Weibull (R-30)
+# --------------------------------------------------------------------------
+def log_uniform(seed, stream, base, n, i0=0, dtype=np.float64):
+    out = np.empty(n, dtype)
+    getattr(lib(), "orc_log_uniform_" + _sfx(dtype))(seed, stream, base, _p(out), i0, n)
+    return out
+
+
+def laplace(seed, stream, base, mu, beta, i0=0, dtype=None):
+    dtype = dtype or mu.dtype
+    mu = _c(mu, dtype); beta = _c(beta, dtype); out = np.empty(mu.shape, dtype)
+    nbad = getattr(lib(), "orc_laplace_" + _sfx(dtype))(seed, stream, base, _p(mu), _p(beta),
+                                                         _p(out), i0, mu.size)
+    return out, int(nbad)
+
+
+def weibull(seed, stream, base, alpha, beta, i0=0, dtype=None):
+    dtype = dtype or alpha.dtype
+    alpha = _c(alpha, dtype); beta = _c(beta, dtype); out = np.empty(alpha.shape, dtype)
+    nbad = getattr(lib(), "orc_weibull_" + _sfx(dtype))(seed, stream, base, _p(alpha),
+                                                         _p(beta), _p(out), i0, alpha.size)
     return out, int(nbad)
 
 

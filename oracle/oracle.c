@@ -245,6 +245,69 @@ DEF_FILLS(float, f32, 0)
 DEF_FILLS(double, f64, 1)
 
 /* ------------------------------------------------------------------------- */
+/* 5b. NEXT row N2: the paper's other irreducible getters       */
+/*     GetLaplace, GetWeibull and the log-uniform buffer GetLogUniform */
+/*     (P:L69).  Algorithms per SPEC S:L231-249 (paper silent, R-30):    */
+/*       log-uniform  l = ln(1-u)                     (1 word, like uniform)   */
+/*       Laplace      x = mu + beta * s * e,  e = -ln(1-u_a), s = -1 iff u_b<1/2 */
+/*                    f32: block i/2, words (2j, 2j+1), j = i mod 2;           */
+/*                    f64: block i, e from u53(w0,w1), s from u53(w2,w3)       */
+/*       Weibull      x = beta * e^(1/alpha),  e = -ln(1-u)   (1 word)        */
+/* ------------------------------------------------------------------------- */
+static double laplace_std_at(uint64_t seed, uint64_t stream, uint64_t base, uint64_t i,
+                             int is_f64)
+{
+    uint32_t w[4];
+    double ua, ub;
+    if (is_f64) {
+        orc_block(seed, stream, base + i, w);
+        ua = orc_u53(w[0], w[1]); ub = orc_u53(w[2], w[3]);
+    } else {
+        orc_block(seed, stream, base + i / 2, w);
+        int j = (int)(i % 2);
+        ua = orc_u24(w[2 * j]); ub = orc_u24(w[2 * j + 1]);
+    }
+    double e = -log(1.0 - ua);
+    return ub < 0.5 ? -e : e;
+}
+
+#define DEF_NEXT(T, SFX, IS64)                                                     \
+ORC_API void orc_log_uniform_##SFX(uint64_t seed, uint64_t stream, uint64_t base,  \
+        T *out, uint64_t i0, uint64_t n)                                           \
+{                                                                                  \
+    for (uint64_t k = 0; k < n; ++k)                                               \
+        out[k] = (T)log(1.0 - std_uniform_at(seed, stream, base, i0 + k, IS64));   \
+}                                                                                  \
+ORC_API uint64_t orc_laplace_##SFX(uint64_t seed, uint64_t stream, uint64_t base,  \
+        const T *mu, const T *beta, T *out, uint64_t i0, uint64_t n)               \
+{                                                                                  \
+    uint64_t nbad = 0;                                                             \
+    for (uint64_t k = 0; k < n; ++k) {                                             \
+        double m = (double)mu[k], b = (double)beta[k];                             \
+        if (!(finite_d(m) && finite_d(b) && b > 0.0)) { out[k] = (T)NAN; ++nbad; continue; } \
+        out[k] = (T)(m + b * laplace_std_at(seed, stream, base, i0 + k, IS64));    \
+    }                                                                              \
+    return nbad;                                                                   \
+}                                                                                  \
+ORC_API uint64_t orc_weibull_##SFX(uint64_t seed, uint64_t stream, uint64_t base,  \
+        const T *alpha, const T *beta, T *out, uint64_t i0, uint64_t n)            \
+{                                                                                  \
+    uint64_t nbad = 0;                                                             \
+    for (uint64_t k = 0; k < n; ++k) {                                             \
+        double a = (double)alpha[k], b = (double)beta[k];                          \
+        if (!(finite_d(a) && finite_d(b) && a > 0.0 && b > 0.0)) {                 \
+            out[k] = (T)NAN; ++nbad; continue;                                     \
+        }                                                                          \
+        double e = -log(1.0 - std_uniform_at(seed, stream, base, i0 + k, IS64));   \
+        out[k] = (T)(b * pow(e, 1.0 / a));                                         \
+    }                                                                              \
+    return nbad;                                                                   \
+}
+
+DEF_NEXT(float, f32, 0)
+DEF_NEXT(double, f64, 1)
+
+/* ------------------------------------------------------------------------- */
 /* 6. Gamma by Marsaglia-Tsang (R-08..R-11).  The paper withholds GetGamma     */
 /*     but names it an irreducible distribution built on the Gaussian  */
 /*    and log-uniform buffers; SPEC states the algorithm        */
