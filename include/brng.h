@@ -24,7 +24,7 @@
  *            cursor by span AT ENQUEUE TIME on the host, so results never
  *            depend on execution timing, grid shape or GPU count.
  *            span = ceil(n/4) for f32 fills and raw words, ceil(n/2) for f64
- *            fills, 256*n for Gamma, 256*n_rows*k for Dirichlet, n_sweeps for
+ *            fills (Laplace: ceil(n/2) f32, n f64), 256*n for Gamma, 256*n_rows*k for Dirichlet, n_sweeps for
  *            Gibbs.  Sample i of a call is a pure function of (seed, stream,
  *            cursor at enqueue, i, the i-th parameters).
  *  Pointers. Arrays are caller-owned, contiguous, any alignment (16-byte
@@ -140,6 +140,27 @@ BRNG_API int brng_gaussian_f32(brng_t h, const float* mu, const float* sigma, fl
 BRNG_API int brng_gaussian_f64(brng_t h, const double* mu, const double* sigma, double* out, uint64_t n);
 BRNG_API int brng_exponential_f32(brng_t h, const float* lambda, float* out, uint64_t n);
 BRNG_API int brng_exponential_f64(brng_t h, const double* lambda, double* out, uint64_t n);
+
+/* ---- NEXT row N2: the paper's other getters (P:L69 GetLogUniform; P:L70
+ * GetLaplace, GetWeibull; algorithms R-30 / SPEC S:L221-249) ----------------
+ *   log-uniform: out[i] = ln(1 - u_i)            (u_i as std_uniform; <= 0)
+ *   Laplace:     out[i] = mu[i] + beta[i] * s * e, e = -ln(1-u_a), s = -1 iff
+ *                u_b < 1/2; valid iff beta > 0, finite.  Two uniforms per
+ *                sample: f32 -- block cursor+floor(i/2), (u_a,u_b) = u24 of
+ *                words (2j, 2j+1), j = i mod 2 (span ceil(n/2)); f64 -- block
+ *                cursor+i, u_a = u53(w0,w1), u_b = u53(w2,w3) (span n).
+ *   Weibull:     out[i] = beta[i] * e^(1/alpha[i]), e = -ln(1-u_i) (shape
+ *                alpha, scale beta); valid iff alpha > 0, beta > 0, finite.
+ * All arrays length n. */
+BRNG_API int brng_log_uniform_f32(brng_t h, float* out, uint64_t n);
+BRNG_API int brng_log_uniform_f64(brng_t h, double* out, uint64_t n);
+BRNG_API int brng_laplace_f32(brng_t h, const float* mu, const float* beta, float* out, uint64_t n);
+BRNG_API int brng_laplace_f64(brng_t h, const double* mu, const double* beta, double* out,
+                              uint64_t n);
+BRNG_API int brng_weibull_f32(brng_t h, const float* alpha, const float* beta, float* out,
+                              uint64_t n);
+BRNG_API int brng_weibull_f64(brng_t h, const double* alpha, const double* beta, double* out,
+                              uint64_t n);
 
 /* ---- Gamma (Marsaglia-Tsang, R-08..R-11) -----------
  * out[i] ~ Gamma(shape alpha[i], scale beta[i]); valid iff alpha>0, beta>0,

@@ -46,6 +46,12 @@ _SIGS = {
     "brng_gaussian_f64": [_H, _vp, _vp, _vp, _u64],
     "brng_exponential_f32": [_H, _vp, _vp, _u64],
     "brng_exponential_f64": [_H, _vp, _vp, _u64],
+    "brng_log_uniform_f32": [_H, _vp, _u64],
+    "brng_log_uniform_f64": [_H, _vp, _u64],
+    "brng_laplace_f32": [_H, _vp, _vp, _vp, _u64],
+    "brng_laplace_f64": [_H, _vp, _vp, _vp, _u64],
+    "brng_weibull_f32": [_H, _vp, _vp, _vp, _u64],
+    "brng_weibull_f64": [_H, _vp, _vp, _vp, _u64],
     "brng_gamma_f32": [_H, _vp, _vp, _vp, _u64, _vp],
     "brng_gamma_f64": [_H, _vp, _vp, _vp, _u64, _vp],
     "brng_dirichlet_f32": [_H, _vp, _u64, _u64, _vp, _vp],
@@ -184,6 +190,30 @@ def brng_exponential_f32(h, lam, out, n):
 
 def brng_exponential_f64(h, lam, out, n):
     return _fill("brng_exponential_f64", h, n, lam, out)
+
+
+def brng_log_uniform_f32(h, out, n):
+    return _fill("brng_log_uniform_f32", h, n, out)
+
+
+def brng_log_uniform_f64(h, out, n):
+    return _fill("brng_log_uniform_f64", h, n, out)
+
+
+def brng_laplace_f32(h, mu, beta, out, n):
+    return _fill("brng_laplace_f32", h, n, mu, beta, out)
+
+
+def brng_laplace_f64(h, mu, beta, out, n):
+    return _fill("brng_laplace_f64", h, n, mu, beta, out)
+
+
+def brng_weibull_f32(h, alpha, beta, out, n):
+    return _fill("brng_weibull_f32", h, n, alpha, beta, out)
+
+
+def brng_weibull_f64(h, alpha, beta, out, n):
+    return _fill("brng_weibull_f64", h, n, alpha, beta, out)
 
 
 def brng_gamma_f32(h, alpha, beta, out, n, trials=None):

@@ -152,6 +152,11 @@ int run(brng_t h, std::vector<Arr>& arrs, uint64_t n_units, uint64_t align, cons
     a.host = a.ptr != nullptr && !is_device_ptr(a.ptr);
     any_host |= a.host;
   }
+  // chunked runs launch on chunk-local [rows][chunk] layouts, so multi-row
+  // DEVICE arrays are staged too (copies use cudaMemcpyDefault / UVA)
+  if (any_host)
+    for (auto& a : arrs)
+      if (a.ptr != nullptr && a.rows > 1) a.host = true;
   if (!any_host) {
     std::vector<void*> d;
     for (auto& a : arrs) d.push_back(const_cast<void*>(a.ptr));
@@ -192,7 +197,7 @@ int run(brng_t h, std::vector<Arr>& arrs, uint64_t n_units, uint64_t align, cons
       if (!a.out && e == cudaSuccess) {
         const char* hp = static_cast<const char*>(a.ptr) + u0 * a.unit_bytes;
         e = cudaMemcpy2DAsync(dp, nu * a.unit_bytes, hp, n_units * a.unit_bytes,
-                              nu * a.unit_bytes, a.rows, cudaMemcpyHostToDevice, h->s_in);
+                              nu * a.unit_bytes, a.rows, cudaMemcpyDefault, h->s_in);
       }
     }
     if (e == cudaSuccess) e = cudaEventRecord(h->ev_in[b], h->s_in);
@@ -205,7 +210,7 @@ int run(brng_t h, std::vector<Arr>& arrs, uint64_t n_units, uint64_t align, cons
       if (!a.host || !a.out) continue;
       char* hp = static_cast<char*>(const_cast<void*>(a.ptr)) + u0 * a.unit_bytes;
       e = cudaMemcpy2DAsync(hp, n_units * a.unit_bytes, d[k], nu * a.unit_bytes,
-                            nu * a.unit_bytes, a.rows, cudaMemcpyDeviceToHost, h->s_out);
+                            nu * a.unit_bytes, a.rows, cudaMemcpyDefault, h->s_out);
     }
     if (e == cudaSuccess) e = cudaEventRecord(h->ev_out[b], h->s_out);
   }
@@ -219,13 +224,15 @@ int run(brng_t h, std::vector<Arr>& arrs, uint64_t n_units, uint64_t align, cons
 int fill_common(brng_t h, int dist, int dtype, const void* p0, const void* p1, void* out,
                 uint64_t n, size_t esize) {
   if (!h || !out) return BRNG_ERR_NULL;
-  if ((dist == brng::kUniform || dist == brng::kGaussian) && (!p0 || !p1)) return BRNG_ERR_NULL;
+  if ((dist == brng::kUniform || dist == brng::kGaussian || dist == brng::kLaplace ||
+       dist == brng::kWeibull) && (!p0 || !p1))
+    return BRNG_ERR_NULL;
   if (dist == brng::kExponential && !p0) return BRNG_ERR_NULL;
   if (n == 0) return BRNG_OK;
   if (!mul_ok(n, esize)) return BRNG_ERR_SIZE;
   int st = check_device(h);
   if (st) return st;
-  const uint64_t per = (dtype == brng::kF64) ? 2 : 4;
+  const uint64_t per = (uint64_t)brng::samples_per_block(dist, dtype);
   uint64_t base;
   if ((st = reserve(h, n, per, 1, &base))) return st;
   std::vector<Arr> arrs = {{p0, esize, false}, {p1, esize, false}, {out, esize, true}};
@@ -409,6 +416,26 @@ int brng_exponential_f32(brng_t h, const float* lambda, float* out, uint64_t n) 
 }
 int brng_exponential_f64(brng_t h, const double* lambda, double* out, uint64_t n) {
   return fill_common(h, brng::kExponential, brng::kF64, lambda, nullptr, out, n, 8);
+}
+
+int brng_log_uniform_f32(brng_t h, float* out, uint64_t n) {
+  return fill_common(h, brng::kLogUniform, brng::kF32, nullptr, nullptr, out, n, 4);
+}
+int brng_log_uniform_f64(brng_t h, double* out, uint64_t n) {
+  return fill_common(h, brng::kLogUniform, brng::kF64, nullptr, nullptr, out, n, 8);
+}
+int brng_laplace_f32(brng_t h, const float* mu, const float* beta, float* out, uint64_t n) {
+  return fill_common(h, brng::kLaplace, brng::kF32, mu, beta, out, n, 4);
+}
+int brng_laplace_f64(brng_t h, const double* mu, const double* beta, double* out, uint64_t n) {
+  return fill_common(h, brng::kLaplace, brng::kF64, mu, beta, out, n, 8);
+}
+int brng_weibull_f32(brng_t h, const float* alpha, const float* beta, float* out, uint64_t n) {
+  return fill_common(h, brng::kWeibull, brng::kF32, alpha, beta, out, n, 4);
+}
+int brng_weibull_f64(brng_t h, const double* alpha, const double* beta, double* out,
+                     uint64_t n) {
+  return fill_common(h, brng::kWeibull, brng::kF64, alpha, beta, out, n, 8);
 }
 
 int brng_gamma_f32(brng_t h, const float* alpha, const float* beta, float* out, uint64_t n,

@@ -6,7 +6,10 @@
 
 namespace brng {
 
-enum Dist : int { kRaw = 0, kStdUniform = 1, kUniform = 2, kGaussian = 3, kExponential = 4 };
+enum Dist : int {
+  kRaw = 0, kStdUniform = 1, kUniform = 2, kGaussian = 3, kExponential = 4,
+  kLogUniform = 5, kLaplace = 6, kWeibull = 7     // NEXT row N2 (R-30)
+};
 enum DType : int { kF32 = 0, kF64 = 1, kU32 = 2 };
 
 struct Ctx {
@@ -18,6 +21,7 @@ struct Ctx {
 };
 
 // K1/K2: raw words, standard uniforms and per-sample-parameter transforms.
+int samples_per_block(int dist, int dtype);
 cudaError_t launch_fill(int dist, int dtype, const void* p0, const void* p1, void* out,
                         uint64_t n, uint64_t base, const Ctx& ctx);
 // K3: Marsaglia-Tsang Gamma with warp compaction.

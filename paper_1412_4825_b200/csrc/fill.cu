@@ -1,11 +1,13 @@
 // fill.cu -- K1/K2: Philox words, standard uniforms and the per-sample
 // transforms of the reducible distributions ("a + (b - a) * x",
-// P:L69 GetUniform/GetGaussian/GetExponential, P:L87-92 parameters read per
-// sample from memory), as ONE fused streaming pass on sm_100a:
+// P:L69 GetUniform/GetGaussian/GetExponential/GetLogUniform
+// parameters read per sample from memory), plus the NEXT-row N2 getters
+// GetLaplace / GetWeibull (algorithms R-30), as ONE fused streaming
+// pass on sm_100a:
 //
-//   Philox4x32-10 block (4 words, registers) -> 4 f32 / 2 f64 standard
-//   deviates -> 128-bit streaming parameter loads -> per-sample transform ->
-//   128-bit streaming store.
+//   Philox4x32-10 block (4 words, registers) -> standard deviates (4 per block
+//   for f32, 2 for f64; Laplace uses two words per sample) -> vector
+//   streaming parameter loads -> per-sample transform -> vector streaming store.
 //
 // This is the BatchRNG idea recast for the GPU: the "buffer" of standard
 // deviates is the four-word Philox block held in registers, refilled by
@@ -21,57 +23,102 @@ constexpr int kThreads = 256;
 
 template <typename T>
 struct FillArgs {
-  const T* p0;   // a | mu | lambda (nullable for raw/std)
-  const T* p1;   // b | sigma
+  const T* p0;   // a | mu | lambda | alpha   (nullable for raw/std/log-uniform)
+  const T* p1;   // b | sigma | beta
   T* out;
   uint64_t n;
   uint64_t base;
   uint64_t stream;
   uint32_t k0, k1;
-  int vec;       // all arrays 16-byte aligned
+  int vec;       // all arrays aligned to the vector width
   unsigned long long* err;
 };
 
-// ---- per-sample transforms (validity -> NaN + count, R-23) -------
 template <int DIST>
-__device__ __forceinline__ float xform(float p0, float p1, float s, uint32_t& bad) {
-  if (DIST == kUniform) {
-    const bool ok = isfinite(p0) && isfinite(p1) && (p0 < p1);
-    bad += !ok;
-    return ok ? fmaf(p1 - p0, s, p0) : __int_as_float(0x7fffffff);
-  } else if (DIST == kGaussian) {
-    const bool ok = isfinite(p0) && isfinite(p1) && (p1 >= 0.0f);
-    bad += !ok;
-    return ok ? fmaf(p1, s, p0) : __int_as_float(0x7fffffff);
-  } else if (DIST == kExponential) {
-    const bool ok = isfinite(p0) && (p0 > 0.0f);
-    bad += !ok;
-    return ok ? (-logf(1.0f - s)) / p0 : __int_as_float(0x7fffffff);
-  }
-  return s;
+constexpr int n_params() {
+  return (DIST == kUniform || DIST == kGaussian || DIST == kLaplace || DIST == kWeibull) ? 2
+         : (DIST == kExponential) ? 1 : 0;
 }
-template <int DIST>
-__device__ __forceinline__ double xform(double p0, double p1, double s, uint32_t& bad) {
-  if (DIST == kUniform) {
+// samples per Philox block
+template <typename T, int DIST>
+constexpr int spb() {
+  return sizeof(T) == 4 ? (DIST == kLaplace ? 2 : 4) : (DIST == kLaplace ? 1 : 2);
+}
+
+// ---- vector load/store of N consecutive T (streaming cache hints) -----------
+template <typename T, int N> struct Vec;
+template <> struct Vec<float, 4> {
+  static __device__ __forceinline__ void ld(const float* p, float v[4]) {
+    const float4 x = __ldcs(reinterpret_cast<const float4*>(p));
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  }
+  static __device__ __forceinline__ void st(float* p, const float v[4]) {
+    __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+  }
+};
+template <> struct Vec<float, 2> {
+  static __device__ __forceinline__ void ld(const float* p, float v[2]) {
+    const float2 x = __ldcs(reinterpret_cast<const float2*>(p));
+    v[0] = x.x; v[1] = x.y;
+  }
+  static __device__ __forceinline__ void st(float* p, const float v[2]) {
+    __stcs(reinterpret_cast<float2*>(p), make_float2(v[0], v[1]));
+  }
+};
+template <> struct Vec<double, 2> {
+  static __device__ __forceinline__ void ld(const double* p, double v[2]) {
+    const double2 x = __ldcs(reinterpret_cast<const double2*>(p));
+    v[0] = x.x; v[1] = x.y;
+  }
+  static __device__ __forceinline__ void st(double* p, const double v[2]) {
+    __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+  }
+};
+template <> struct Vec<double, 1> {
+  static __device__ __forceinline__ void ld(const double* p, double v[1]) { v[0] = __ldcs(p); }
+  static __device__ __forceinline__ void st(double* p, const double v[1]) { __stcs(p, v[0]); }
+};
+
+__device__ __forceinline__ float fnan() { return __int_as_float(0x7fffffff); }
+__device__ __forceinline__ double dnan() { return __longlong_as_double(0x7ff8000000000000ll); }
+__device__ __forceinline__ float flog(float x) { return logf(x); }
+__device__ __forceinline__ double flog(double x) { return log(x); }
+__device__ __forceinline__ float fexp(float x) { return expf(x); }
+__device__ __forceinline__ double fexp(double x) { return exp(x); }
+
+// ---- per-sample transforms (validity -> NaN + count, R-23) --------
+template <int DIST, typename T>
+__device__ __forceinline__ T xform(T p0, T p1, T s, uint32_t& bad) {
+  const T nanv = sizeof(T) == 4 ? (T)fnan() : (T)dnan();
+  if (DIST == kUniform) {                 // a + (b - a) u
     const bool ok = isfinite(p0) && isfinite(p1) && (p0 < p1);
     bad += !ok;
-    return ok ? fma(p1 - p0, s, p0) : __longlong_as_double(0x7ff8000000000000ll);
-  } else if (DIST == kGaussian) {
-    const bool ok = isfinite(p0) && isfinite(p1) && (p1 >= 0.0);
+    return ok ? fma(p1 - p0, s, p0) : nanv;
+  } else if (DIST == kGaussian) {         // mu + sigma z
+    const bool ok = isfinite(p0) && isfinite(p1) && (p1 >= T(0));
     bad += !ok;
-    return ok ? fma(p1, s, p0) : __longlong_as_double(0x7ff8000000000000ll);
-  } else if (DIST == kExponential) {
-    const bool ok = isfinite(p0) && (p0 > 0.0);
+    return ok ? fma(p1, s, p0) : nanv;
+  } else if (DIST == kExponential) {      // e / lambda  (rate, R-07)
+    const bool ok = isfinite(p0) && (p0 > T(0));
     bad += !ok;
-    return ok ? (-log(1.0 - s)) / p0 : __longlong_as_double(0x7ff8000000000000ll);
+    return ok ? s / p0 : nanv;
+  } else if (DIST == kLaplace) {          // mu + beta (+-e)
+    const bool ok = isfinite(p0) && isfinite(p1) && (p1 > T(0));
+    bad += !ok;
+    return ok ? fma(p1, s, p0) : nanv;
+  } else if (DIST == kWeibull) {          // beta e^(1/alpha)
+    const bool ok = isfinite(p0) && isfinite(p1) && (p0 > T(0)) && (p1 > T(0));
+    bad += !ok;
+    return ok ? p1 * fexp(flog(s) / p0) : nanv;
   }
   return s;
 }
 
-// ---- standard deviates of one block ----------------------------------------
-// f32: four u24 uniforms, or two Box-Muller pairs (R-06).
+// ---- standard deviates of one block -----------------------------------------
+// f32: 4 x u24 words (uniform / exponential / log-uniform / Weibull), two
+// Box-Muller pairs (R-06) or two Laplace (exponential, sign) pairs (R-30).
 template <int DIST>
-__device__ __forceinline__ void std4(uint4 w, float s[4]) {
+__device__ __forceinline__ void std_block(uint4 w, float* s) {
   if (DIST == kGaussian) {
     float sn, cs;
     const float r0 = sqrtf(-2.0f * logf(1.0f - u24(w.x)));
@@ -80,93 +127,77 @@ __device__ __forceinline__ void std4(uint4 w, float s[4]) {
     const float r1 = sqrtf(-2.0f * logf(1.0f - u24(w.z)));
     sincospif(2.0f * u24(w.w), &sn, &cs);
     s[2] = r1 * cs; s[3] = r1 * sn;
+  } else if (DIST == kLaplace) {
+    const float e0 = -logf(1.0f - u24(w.x)), e1 = -logf(1.0f - u24(w.z));
+    s[0] = u24(w.y) < 0.5f ? -e0 : e0;
+    s[1] = u24(w.w) < 0.5f ? -e1 : e1;
   } else {
-    s[0] = u24(w.x); s[1] = u24(w.y); s[2] = u24(w.z); s[3] = u24(w.w);
+    const float u[4] = {u24(w.x), u24(w.y), u24(w.z), u24(w.w)};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (DIST == kExponential || DIST == kWeibull) s[k] = -logf(1.0f - u[k]);
+      else if (DIST == kLogUniform) s[k] = logf(1.0f - u[k]);
+      else s[k] = u[k];
+    }
   }
 }
-// f64: two u53 uniforms, or one Box-Muller pair.
+// f64: 2 x u53 (uniform / exponential / log-uniform / Weibull), one Box-Muller
+// pair, or one Laplace sample.
 template <int DIST>
-__device__ __forceinline__ void std2(uint4 w, double s[2]) {
+__device__ __forceinline__ void std_block(uint4 w, double* s) {
   if (DIST == kGaussian) {
     double sn, cs;
     const double r = sqrt(-2.0 * log(1.0 - u53(w.x, w.y)));
     sincospi(2.0 * u53(w.z, w.w), &sn, &cs);
     s[0] = r * cs; s[1] = r * sn;
+  } else if (DIST == kLaplace) {
+    const double e = -log(1.0 - u53(w.x, w.y));
+    s[0] = u53(w.z, w.w) < 0.5 ? -e : e;
   } else {
-    s[0] = u53(w.x, w.y); s[1] = u53(w.z, w.w);
+    const double u[2] = {u53(w.x, w.y), u53(w.z, w.w)};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (DIST == kExponential || DIST == kWeibull) s[k] = -log(1.0 - u[k]);
+      else if (DIST == kLogUniform) s[k] = log(1.0 - u[k]);
+      else s[k] = u[k];
+    }
   }
 }
 
 // ---- kernels ------------------------------------------------------------------
-template <int DIST>
-__global__ void __launch_bounds__(kThreads) fill_f32_kernel(FillArgs<float> a) {
-  const uint64_t nblk = (a.n + 3) >> 2;
+template <typename T, int DIST>
+__global__ void __launch_bounds__(kThreads) fill_kernel(FillArgs<T> a) {
+  constexpr int S = spb<T, DIST>();
+  constexpr int NP = n_params<DIST>();
+  const uint64_t nblk = (a.n + S - 1) / S;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   uint32_t bad = 0;
   for (uint64_t j = (uint64_t)blockIdx.x * kThreads + threadIdx.x; j < nblk; j += stride) {
     const uint4 w = philox_block(a.base + j, a.stream, a.k0, a.k1);
-    float s[4];
-    std4<DIST>(w, s);
-    const uint64_t i0 = j << 2;
-    if (a.vec && i0 + 4 <= a.n) {
-      float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0;
-      if (DIST == kUniform || DIST == kGaussian || DIST == kExponential)
-        p0 = __ldcs(reinterpret_cast<const float4*>(a.p0) + j);
-      if (DIST == kUniform || DIST == kGaussian)
-        p1 = __ldcs(reinterpret_cast<const float4*>(a.p1) + j);
-      float4 o;
-      o.x = xform<DIST>(p0.x, p1.x, s[0], bad);
-      o.y = xform<DIST>(p0.y, p1.y, s[1], bad);
-      o.z = xform<DIST>(p0.z, p1.z, s[2], bad);
-      o.w = xform<DIST>(p0.w, p1.w, s[3], bad);
-      __stcs(reinterpret_cast<float4*>(a.out) + j, o);
+    T s[S];
+    std_block<DIST>(w, s);
+    const uint64_t i0 = j * S;
+    T p0[S], p1[S], o[S];
+    if (a.vec && i0 + S <= a.n) {
+      if (NP >= 1) Vec<T, S>::ld(a.p0 + i0, p0);
+      if (NP >= 2) Vec<T, S>::ld(a.p1 + i0, p1);
+#pragma unroll
+      for (int k = 0; k < S; ++k)
+        o[k] = xform<DIST>(NP >= 1 ? p0[k] : T(0), NP >= 2 ? p1[k] : T(0), s[k], bad);
+      Vec<T, S>::st(a.out + i0, o);
     } else {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < S; ++k) {
         const uint64_t i = i0 + k;
         if (i < a.n) {
-          const float p0 = (DIST >= kUniform) ? a.p0[i] : 0.f;
-          const float p1 = (DIST == kUniform || DIST == kGaussian) ? a.p1[i] : 0.f;
-          a.out[i] = xform<DIST>(p0, p1, s[k], bad);
+          const T q0 = NP >= 1 ? a.p0[i] : T(0);
+          const T q1 = NP >= 2 ? a.p1[i] : T(0);
+          a.out[i] = xform<DIST>(q0, q1, s[k], bad);
         }
       }
     }
   }
-  if (DIST >= kUniform) flush_errors(a.err, bad);
-}
-
-template <int DIST>
-__global__ void __launch_bounds__(kThreads) fill_f64_kernel(FillArgs<double> a) {
-  const uint64_t nblk = (a.n + 1) >> 1;
-  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-  uint32_t bad = 0;
-  for (uint64_t j = (uint64_t)blockIdx.x * kThreads + threadIdx.x; j < nblk; j += stride) {
-    const uint4 w = philox_block(a.base + j, a.stream, a.k0, a.k1);
-    double s[2];
-    std2<DIST>(w, s);
-    const uint64_t i0 = j << 1;
-    if (a.vec && i0 + 2 <= a.n) {
-      double2 p0 = make_double2(0.0, 0.0), p1 = p0;
-      if (DIST >= kUniform) p0 = __ldcs(reinterpret_cast<const double2*>(a.p0) + j);
-      if (DIST == kUniform || DIST == kGaussian)
-        p1 = __ldcs(reinterpret_cast<const double2*>(a.p1) + j);
-      double2 o;
-      o.x = xform<DIST>(p0.x, p1.x, s[0], bad);
-      o.y = xform<DIST>(p0.y, p1.y, s[1], bad);
-      __stcs(reinterpret_cast<double2*>(a.out) + j, o);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const uint64_t i = i0 + k;
-        if (i < a.n) {
-          const double p0 = (DIST >= kUniform) ? a.p0[i] : 0.0;
-          const double p1 = (DIST == kUniform || DIST == kGaussian) ? a.p1[i] : 0.0;
-          a.out[i] = xform<DIST>(p0, p1, s[k], bad);
-        }
-      }
-    }
-  }
-  if (DIST >= kUniform) flush_errors(a.err, bad);
+  if (NP > 0) flush_errors(a.err, bad);
 }
 
 __global__ void __launch_bounds__(kThreads) raw_u32_kernel(FillArgs<uint32_t> a) {
@@ -185,7 +216,9 @@ __global__ void __launch_bounds__(kThreads) raw_u32_kernel(FillArgs<uint32_t> a)
   }
 }
 
-inline bool aligned16(const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; }
+inline bool aligned(const void* p, uintptr_t bytes) {
+  return p == nullptr || ((uintptr_t)p & (bytes - 1)) == 0;
+}
 
 inline unsigned grid_for(uint64_t nblk, const Ctx& ctx) {
   const uint64_t want = (nblk + kThreads - 1) / kThreads;
@@ -193,49 +226,45 @@ inline unsigned grid_for(uint64_t nblk, const Ctx& ctx) {
   return (unsigned)(want < cap ? (want ? want : 1) : cap);
 }
 
-template <typename T>
-cudaError_t run_typed(int dist, const T* p0, const T* p1, T* out, uint64_t n, uint64_t base,
-                      const Ctx& ctx);
-
-template <>
-cudaError_t run_typed<float>(int dist, const float* p0, const float* p1, float* out, uint64_t n,
-                             uint64_t base, const Ctx& ctx) {
-  FillArgs<float> a{p0, p1, out, n, base, ctx.stream_id, ctx.k0, ctx.k1,
-                    aligned16(p0) && aligned16(p1) && aligned16(out), ctx.err};
-  const unsigned g = grid_for((n + 3) >> 2, ctx);
-  switch (dist) {
-    case kStdUniform: fill_f32_kernel<kStdUniform><<<g, kThreads, 0, ctx.stream>>>(a); break;
-    case kUniform: fill_f32_kernel<kUniform><<<g, kThreads, 0, ctx.stream>>>(a); break;
-    case kGaussian: fill_f32_kernel<kGaussian><<<g, kThreads, 0, ctx.stream>>>(a); break;
-    case kExponential: fill_f32_kernel<kExponential><<<g, kThreads, 0, ctx.stream>>>(a); break;
-    default: return cudaErrorInvalidValue;
-  }
+template <typename T, int DIST>
+cudaError_t run_dist(const T* p0, const T* p1, T* out, uint64_t n, uint64_t base,
+                     const Ctx& ctx) {
+  constexpr int S = spb<T, DIST>();
+  const uintptr_t vb = sizeof(T) * S;
+  FillArgs<T> a{p0, p1, out, n, base, ctx.stream_id, ctx.k0, ctx.k1,
+                aligned(p0, vb) && aligned(p1, vb) && aligned(out, vb), ctx.err};
+  fill_kernel<T, DIST><<<grid_for((n + S - 1) / S, ctx), kThreads, 0, ctx.stream>>>(a);
   return cudaGetLastError();
 }
 
-template <>
-cudaError_t run_typed<double>(int dist, const double* p0, const double* p1, double* out,
-                              uint64_t n, uint64_t base, const Ctx& ctx) {
-  FillArgs<double> a{p0, p1, out, n, base, ctx.stream_id, ctx.k0, ctx.k1,
-                     aligned16(p0) && aligned16(p1) && aligned16(out), ctx.err};
-  const unsigned g = grid_for((n + 1) >> 1, ctx);
+template <typename T>
+cudaError_t run_typed(int dist, const T* p0, const T* p1, T* out, uint64_t n, uint64_t base,
+                      const Ctx& ctx) {
   switch (dist) {
-    case kStdUniform: fill_f64_kernel<kStdUniform><<<g, kThreads, 0, ctx.stream>>>(a); break;
-    case kUniform: fill_f64_kernel<kUniform><<<g, kThreads, 0, ctx.stream>>>(a); break;
-    case kGaussian: fill_f64_kernel<kGaussian><<<g, kThreads, 0, ctx.stream>>>(a); break;
-    case kExponential: fill_f64_kernel<kExponential><<<g, kThreads, 0, ctx.stream>>>(a); break;
+    case kStdUniform: return run_dist<T, kStdUniform>(p0, p1, out, n, base, ctx);
+    case kUniform: return run_dist<T, kUniform>(p0, p1, out, n, base, ctx);
+    case kGaussian: return run_dist<T, kGaussian>(p0, p1, out, n, base, ctx);
+    case kExponential: return run_dist<T, kExponential>(p0, p1, out, n, base, ctx);
+    case kLogUniform: return run_dist<T, kLogUniform>(p0, p1, out, n, base, ctx);
+    case kLaplace: return run_dist<T, kLaplace>(p0, p1, out, n, base, ctx);
+    case kWeibull: return run_dist<T, kWeibull>(p0, p1, out, n, base, ctx);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 }  // namespace
+
+int samples_per_block(int dist, int dtype) {
+  if (dist == kRaw) return 4;
+  if (dtype == kF64) return dist == kLaplace ? 1 : 2;
+  return dist == kLaplace ? 2 : 4;
+}
 
 cudaError_t launch_fill(int dist, int dtype, const void* p0, const void* p1, void* out,
                         uint64_t n, uint64_t base, const Ctx& ctx) {
   if (dist == kRaw) {
     FillArgs<uint32_t> a{nullptr, nullptr, static_cast<uint32_t*>(out), n, base, ctx.stream_id,
-                         ctx.k0, ctx.k1, aligned16(out), ctx.err};
+                         ctx.k0, ctx.k1, aligned(out, 16), ctx.err};
     raw_u32_kernel<<<grid_for((n + 3) >> 2, ctx), kThreads, 0, ctx.stream>>>(a);
     return cudaGetLastError();
   }

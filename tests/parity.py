@@ -53,6 +53,28 @@ def fill_reference(dist, seed, stream, base, params, i0, dtype):
         (lam,) = params
         ref, _ = oracle.exponential(seed, stream, base, lam, i0=i0, dtype=dtype)
         scale = np.abs(ref.astype(np.float64))
+    elif dist == "log_uniform":
+        (n,) = params
+        ref = oracle.log_uniform(seed, stream, base, n, i0=i0, dtype=dtype)
+        scale = np.abs(ref.astype(np.float64))
+    elif dist == "laplace":
+        mu, beta = params
+        ref, _ = oracle.laplace(seed, stream, base, mu, beta, i0=i0, dtype=dtype)
+        s, _ = oracle.laplace(seed, stream, base, np.zeros(len(mu), dtype), np.ones(len(mu), dtype),
+                              i0=i0, dtype=dtype)
+        scale = np.abs(mu.astype(np.float64)) + np.abs(beta.astype(np.float64) * s.astype(np.float64))
+    elif dist == "weibull":
+        alpha, beta = params
+        ref, _ = oracle.weibull(seed, stream, base, alpha, beta, i0=i0, dtype=dtype)
+        # x = beta e^(1/alpha): a relative error in e (or in ln e) is amplified
+        # by 1/alpha (and |ln e| / alpha), so the scale carries that condition
+        e, _ = oracle.exponential(seed, stream, base, np.ones(len(alpha), dtype), i0=i0,
+                                  dtype=dtype)
+        with np.errstate(divide="ignore"):
+            lne = np.abs(np.log(e.astype(np.float64)))
+        lne[~np.isfinite(lne)] = 0.0
+        cond = np.maximum(1.0, (1.0 + lne) / alpha.astype(np.float64))
+        scale = np.abs(ref.astype(np.float64)) * cond
     else:
         raise ValueError(dist)
     return ref, scale

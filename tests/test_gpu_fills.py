@@ -206,3 +206,62 @@ def test_host_pipeline_multi_chunk_equals_device():
         out_m = np.empty(n, np.float32)
         B.brng_gaussian_f32(h, p["mu"].to(dev()), p["sigma"].to(dev()), out_m, n)
     assert np.array_equal(out_m, out_h)
+
+
+# ---- NEXT row N2: log-uniform, Laplace, Weibull ---------------
+def _next_params(dist, n, dtype, seed=13):
+    import math
+    g = torch.Generator().manual_seed(seed)
+    td = torch.float32 if dtype == np.float32 else torch.float64
+    u = lambda lo, hi: (lo + (hi - lo) * torch.rand(n, generator=g, dtype=torch.float64))  # noqa
+    lu = lambda lo, hi: torch.exp(math.log(lo) + u(0, 1) * (math.log(hi) - math.log(lo)))  # noqa
+    if dist == "laplace":
+        return [u(-10, 10).to(td), lu(1e-3, 1e3).to(td)]
+    return [lu(0.2, 5).to(td), lu(0.1, 10).to(td)]          # weibull alpha, beta
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n", [1, 3, 4099, 100_003])
+def test_next_row_n2_parity(dtype, n):
+    td = torch.float32 if dtype == np.float32 else torch.float64
+    sfx = "f32" if dtype == np.float32 else "f64"
+    for off in (0, 1):
+        with handle(13, 2, 77) as h:
+            out = empty(n, td, off)
+            getattr(B, f"brng_log_uniform_{sfx}")(h, out, n)
+            ref, sc = parity.fill_reference("log_uniform", 13, 2, 77, [n], 0, dtype)
+            parity.check_close(out, ref, sc, dtype, f"log_uniform {sfx} n={n}")
+            per = 2 if dtype == np.float64 else 4
+            assert B.brng_get_offset(h) == 77 + (n + per - 1) // per
+        for dist in ("laplace", "weibull"):
+            params = _next_params(dist, n, dtype)
+            with handle(13, 2, 77) as h:
+                out = empty(n, td, off)
+                getattr(B, f"brng_{dist}_{sfx}")(h, *[to_dev(p, off) for p in params], out, n)
+                assert B.brng_device_errors(h) == 0
+                pd = {"laplace": 1 if dtype == np.float64 else 2}.get(dist, per)
+                assert B.brng_get_offset(h) == 77 + (n + pd - 1) // pd
+            ref, sc = parity.fill_reference(dist, 13, 2, 77, [p.numpy() for p in params], 0, dtype)
+            parity.check_close(out, ref, sc, dtype, f"{dist} {sfx} n={n} off={off}")
+
+
+def test_next_row_n2_statistics_and_invalid():
+    from tests.stats_util import assert_ks_uniform
+    n = 1 << 20
+    mu, b = _next_params("laplace", n, np.float32)
+    al, be = _next_params("weibull", n, np.float32, seed=14)
+    with handle(21) as h:
+        x = torch.empty(n, device=dev())
+        B.brng_laplace_f32(h, mu.to(dev()), b.to(dev()), x, n)
+        w = torch.empty(n, device=dev())
+        B.brng_weibull_f32(h, al.to(dev()), be.to(dev()), w, n)
+        bad = torch.tensor([0.0, -1.0, float("nan"), 2.0], device=dev())
+        o = torch.empty(4, device=dev())
+        B.brng_weibull_f32(h, bad, torch.ones(4, device=dev()), o, 4)
+        assert B.brng_device_errors(h) == 3
+        assert torch.isnan(o[:3]).all().item() and not torch.isnan(o[3])
+    z = (x.double().cpu().numpy() - mu.double().numpy()) / b.double().numpy()
+    assert_ks_uniform(np.where(z < 0, 0.5 * np.exp(z), 1 - 0.5 * np.exp(-z)), "GPU Laplace PIT")
+    wv = w.double().cpu().numpy()
+    assert_ks_uniform(-np.expm1(-(wv / be.double().numpy()) ** al.double().numpy()),
+                      "GPU Weibull PIT")
