@@ -162,6 +162,25 @@ BRNG_API int brng_weibull_f32(brng_t h, const float* alpha, const float* beta, f
 BRNG_API int brng_weibull_f64(brng_t h, const double* alpha, const double* beta, double* out,
                               uint64_t n);
 
+/* ---- fixed-parameter batch fill (NEXT row N1: the paper's "VSL-Batch"
+ * column) --------------------------------
+ * Every sample i uses the same parameters (p0, p1) -- no parameter arrays,
+ * 4 (f32) / 8 (f64) bytes per sample.  dist: BRNG_DIST_UNIFORM (a, b),
+ * _GAUSSIAN (mu, sigma), _EXPONENTIAL (lambda, unused), _LAPLACE (mu, beta),
+ * _WEIBULL (alpha, beta); dtype: BRNG_DTYPE_F32 / _F64.  Same counters, span
+ * and values as the per-sample call with constant parameter arrays.  An
+ * unknown dist/dtype returns BRNG_ERR_PARAM; invalid p0/p1 make every output
+ * NaN and are counted per sample. */
+#define BRNG_DIST_UNIFORM 2
+#define BRNG_DIST_GAUSSIAN 3
+#define BRNG_DIST_EXPONENTIAL 4
+#define BRNG_DIST_LAPLACE 6
+#define BRNG_DIST_WEIBULL 7
+#define BRNG_DTYPE_F32 0
+#define BRNG_DTYPE_F64 1
+BRNG_API int brng_batch_fill(brng_t h, int dist, int dtype, double p0, double p1, void* out,
+                             uint64_t n);
+
 /* ---- Gamma (Marsaglia-Tsang, R-08..R-11) -----------
  * out[i] ~ Gamma(shape alpha[i], scale beta[i]); valid iff alpha>0, beta>0,
  * finite.  alpha' = alpha<1 ? alpha+1 : alpha; d = alpha' - 1/3;

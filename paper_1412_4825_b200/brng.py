@@ -46,6 +46,7 @@ _SIGS = {
     "brng_gaussian_f64": [_H, _vp, _vp, _vp, _u64],
     "brng_exponential_f32": [_H, _vp, _vp, _u64],
     "brng_exponential_f64": [_H, _vp, _vp, _u64],
+    "brng_batch_fill": [_H, _int, _int, C.c_double, C.c_double, _vp, _u64],
     "brng_log_uniform_f32": [_H, _vp, _u64],
     "brng_log_uniform_f64": [_H, _vp, _u64],
     "brng_laplace_f32": [_H, _vp, _vp, _vp, _u64],
@@ -190,6 +191,15 @@ def brng_exponential_f32(h, lam, out, n):
 
 def brng_exponential_f64(h, lam, out, n):
     return _fill("brng_exponential_f64", h, n, lam, out)
+
+
+DIST = {"uniform": 2, "gaussian": 3, "exponential": 4, "laplace": 6, "weibull": 7}
+DTYPE = {"f32": 0, "f64": 1}
+
+
+def brng_batch_fill(h, dist, dtype, p0, p1, out, n):
+    """Fixed-parameter fill; dist/dtype are the BRNG_DIST_*/BRNG_DTYPE_* codes."""
+    return _check("brng_batch_fill", _lib.brng_batch_fill(h, dist, dtype, p0, p1, _ptr(out), n))
 
 
 def brng_log_uniform_f32(h, out, n):

@@ -245,6 +245,31 @@ int fill_common(brng_t h, int dist, int dtype, const void* p0, const void* p1, v
   return BRNG_OK;
 }
 
+// Fixed-parameter batch fill (the paper's VSL-Batch scenario).
+int batch_common(brng_t h, int dist, int dtype, double p0, double p1, void* out, uint64_t n) {
+  if (!h || !out) return BRNG_ERR_NULL;
+  if (dist < brng::kUniform || dist > brng::kWeibull || dist == brng::kLogUniform)
+    return BRNG_ERR_PARAM;
+  if (dtype != brng::kF32 && dtype != brng::kF64) return BRNG_ERR_PARAM;
+  if (n == 0) return BRNG_OK;
+  const size_t esize = dtype == brng::kF64 ? 8 : 4;
+  if (!mul_ok(n, esize)) return BRNG_ERR_SIZE;
+  int st = check_device(h);
+  if (st) return st;
+  const uint64_t per = (uint64_t)brng::samples_per_block(dist, dtype);
+  uint64_t base;
+  if ((st = reserve(h, n, per, 1, &base))) return st;
+  std::vector<Arr> arrs = {{out, esize, true}};
+  const Ctx ctx = make_ctx(h);
+  const double sc[2] = {p0, p1};
+  st = run(h, arrs, n, per, [&](uint64_t u0, uint64_t nu, const std::vector<void*>& d, bool) {
+    return brng::launch_fill(dist, dtype, nullptr, nullptr, d[0], nu, base + u0 / per, ctx, sc);
+  });
+  if (st) return st;
+  commit(h, n, per, 1);
+  return BRNG_OK;
+}
+
 int gamma_common(brng_t h, int dtype, const void* alpha, const void* beta, void* out,
                  uint64_t n, uint8_t* trials, size_t esize) {
   if (!h || !alpha || !beta || !out) return BRNG_ERR_NULL;
@@ -416,6 +441,11 @@ int brng_exponential_f32(brng_t h, const float* lambda, float* out, uint64_t n) 
 }
 int brng_exponential_f64(brng_t h, const double* lambda, double* out, uint64_t n) {
   return fill_common(h, brng::kExponential, brng::kF64, lambda, nullptr, out, n, 8);
+}
+
+int brng_batch_fill(brng_t h, int dist, int dtype, double p0, double p1, void* out,
+                    uint64_t n) {
+  return batch_common(h, dist, dtype, p0, p1, out, n);
 }
 
 int brng_log_uniform_f32(brng_t h, float* out, uint64_t n) {

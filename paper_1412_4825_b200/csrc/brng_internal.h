@@ -22,8 +22,10 @@ struct Ctx {
 
 // K1/K2: raw words, standard uniforms and per-sample-parameter transforms.
 int samples_per_block(int dist, int dtype);
+// scalars != nullptr: fixed parameters scalars[0..1] for every sample (batch).
 cudaError_t launch_fill(int dist, int dtype, const void* p0, const void* p1, void* out,
-                        uint64_t n, uint64_t base, const Ctx& ctx);
+                        uint64_t n, uint64_t base, const Ctx& ctx,
+                        const double* scalars = nullptr);
 // K3: Marsaglia-Tsang Gamma with warp compaction.
 cudaError_t launch_gamma(int dtype, const void* alpha, const void* beta, void* out,
                          uint8_t* trials, uint64_t n, uint64_t base, const Ctx& ctx);

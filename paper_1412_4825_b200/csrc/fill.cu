@@ -32,6 +32,7 @@ struct FillArgs {
   uint32_t k0, k1;
   int vec;       // all arrays aligned to the vector width
   unsigned long long* err;
+  T s0, s1;      // SCALAR mode: fixed parameters (the paper's VSL-Batch case)
 };
 
 template <int DIST>
@@ -165,10 +166,12 @@ __device__ __forceinline__ void std_block(uint4 w, double* s) {
 }
 
 // ---- kernels ------------------------------------------------------------------
-template <typename T, int DIST>
+// SCALAR: every sample uses the fixed parameters (s0, s1) -- the fixed-
+// parameter "Batch" scenario of the paper's Fig. 2, 4 B/sample.
+template <typename T, int DIST, bool SCALAR = false>
 __global__ void __launch_bounds__(kThreads) fill_kernel(FillArgs<T> a) {
   constexpr int S = spb<T, DIST>();
-  constexpr int NP = n_params<DIST>();
+  constexpr int NP = SCALAR ? 0 : n_params<DIST>();
   const uint64_t nblk = (a.n + S - 1) / S;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   uint32_t bad = 0;
@@ -183,21 +186,22 @@ __global__ void __launch_bounds__(kThreads) fill_kernel(FillArgs<T> a) {
       if (NP >= 2) Vec<T, S>::ld(a.p1 + i0, p1);
 #pragma unroll
       for (int k = 0; k < S; ++k)
-        o[k] = xform<DIST>(NP >= 1 ? p0[k] : T(0), NP >= 2 ? p1[k] : T(0), s[k], bad);
+        o[k] = SCALAR ? xform<DIST>(a.s0, a.s1, s[k], bad)
+                      : xform<DIST>(NP >= 1 ? p0[k] : T(0), NP >= 2 ? p1[k] : T(0), s[k], bad);
       Vec<T, S>::st(a.out + i0, o);
     } else {
 #pragma unroll
       for (int k = 0; k < S; ++k) {
         const uint64_t i = i0 + k;
         if (i < a.n) {
-          const T q0 = NP >= 1 ? a.p0[i] : T(0);
-          const T q1 = NP >= 2 ? a.p1[i] : T(0);
+          const T q0 = SCALAR ? a.s0 : (NP >= 1 ? a.p0[i] : T(0));
+          const T q1 = SCALAR ? a.s1 : (NP >= 2 ? a.p1[i] : T(0));
           a.out[i] = xform<DIST>(q0, q1, s[k], bad);
         }
       }
     }
   }
-  if (NP > 0) flush_errors(a.err, bad);
+  if (SCALAR || NP > 0) flush_errors(a.err, bad);
 }
 
 __global__ void __launch_bounds__(kThreads) raw_u32_kernel(FillArgs<uint32_t> a) {
@@ -228,26 +232,33 @@ inline unsigned grid_for(uint64_t nblk, const Ctx& ctx) {
 
 template <typename T, int DIST>
 cudaError_t run_dist(const T* p0, const T* p1, T* out, uint64_t n, uint64_t base,
-                     const Ctx& ctx) {
+                     const Ctx& ctx, const double* scalars) {
   constexpr int S = spb<T, DIST>();
   const uintptr_t vb = sizeof(T) * S;
   FillArgs<T> a{p0, p1, out, n, base, ctx.stream_id, ctx.k0, ctx.k1,
-                aligned(p0, vb) && aligned(p1, vb) && aligned(out, vb), ctx.err};
-  fill_kernel<T, DIST><<<grid_for((n + S - 1) / S, ctx), kThreads, 0, ctx.stream>>>(a);
+                aligned(p0, vb) && aligned(p1, vb) && aligned(out, vb), ctx.err, T(0), T(0)};
+  const unsigned g = grid_for((n + S - 1) / S, ctx);
+  if (scalars) {
+    a.s0 = (T)scalars[0];
+    a.s1 = (T)scalars[1];
+    fill_kernel<T, DIST, true><<<g, kThreads, 0, ctx.stream>>>(a);
+  } else {
+    fill_kernel<T, DIST, false><<<g, kThreads, 0, ctx.stream>>>(a);
+  }
   return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t run_typed(int dist, const T* p0, const T* p1, T* out, uint64_t n, uint64_t base,
-                      const Ctx& ctx) {
+                      const Ctx& ctx, const double* sc) {
   switch (dist) {
-    case kStdUniform: return run_dist<T, kStdUniform>(p0, p1, out, n, base, ctx);
-    case kUniform: return run_dist<T, kUniform>(p0, p1, out, n, base, ctx);
-    case kGaussian: return run_dist<T, kGaussian>(p0, p1, out, n, base, ctx);
-    case kExponential: return run_dist<T, kExponential>(p0, p1, out, n, base, ctx);
-    case kLogUniform: return run_dist<T, kLogUniform>(p0, p1, out, n, base, ctx);
-    case kLaplace: return run_dist<T, kLaplace>(p0, p1, out, n, base, ctx);
-    case kWeibull: return run_dist<T, kWeibull>(p0, p1, out, n, base, ctx);
+    case kStdUniform: return run_dist<T, kStdUniform>(p0, p1, out, n, base, ctx, nullptr);
+    case kUniform: return run_dist<T, kUniform>(p0, p1, out, n, base, ctx, sc);
+    case kGaussian: return run_dist<T, kGaussian>(p0, p1, out, n, base, ctx, sc);
+    case kExponential: return run_dist<T, kExponential>(p0, p1, out, n, base, ctx, sc);
+    case kLogUniform: return run_dist<T, kLogUniform>(p0, p1, out, n, base, ctx, nullptr);
+    case kLaplace: return run_dist<T, kLaplace>(p0, p1, out, n, base, ctx, sc);
+    case kWeibull: return run_dist<T, kWeibull>(p0, p1, out, n, base, ctx, sc);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -261,7 +272,7 @@ int samples_per_block(int dist, int dtype) {
 }
 
 cudaError_t launch_fill(int dist, int dtype, const void* p0, const void* p1, void* out,
-                        uint64_t n, uint64_t base, const Ctx& ctx) {
+                        uint64_t n, uint64_t base, const Ctx& ctx, const double* scalars) {
   if (dist == kRaw) {
     FillArgs<uint32_t> a{nullptr, nullptr, static_cast<uint32_t*>(out), n, base, ctx.stream_id,
                          ctx.k0, ctx.k1, aligned(out, 16), ctx.err};
@@ -270,9 +281,9 @@ cudaError_t launch_fill(int dist, int dtype, const void* p0, const void* p1, voi
   }
   if (dtype == kF32)
     return run_typed<float>(dist, static_cast<const float*>(p0), static_cast<const float*>(p1),
-                            static_cast<float*>(out), n, base, ctx);
+                            static_cast<float*>(out), n, base, ctx, scalars);
   return run_typed<double>(dist, static_cast<const double*>(p0), static_cast<const double*>(p1),
-                           static_cast<double*>(out), n, base, ctx);
+                           static_cast<double*>(out), n, base, ctx, scalars);
 }
 
 }  // namespace brng

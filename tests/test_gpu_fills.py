@@ -265,3 +265,29 @@ def test_next_row_n2_statistics_and_invalid():
     wv = w.double().cpu().numpy()
     assert_ks_uniform(-np.expm1(-(wv / be.double().numpy()) ** al.double().numpy()),
                       "GPU Weibull PIT")
+
+
+def test_batch_fill_equals_constant_arrays():
+    # the fixed-parameter batch fill (N1, VSL-Batch analogue) draws the same
+    # counters and applies the same transform as the per-sample call
+    n = 100_003
+    for dist, (p0, p1) in {"uniform": (-1.0, 2.5), "gaussian": (1.0, 3.0),
+                           "exponential": (0.5, 0.0), "laplace": (2.0, 0.25),
+                           "weibull": (1.5, 2.0)}.items():
+        for dt, td, code in ((np.float32, torch.float32, 0), (np.float64, torch.float64, 1)):
+            with handle(31, 4, 9) as h:
+                ob = torch.empty(n, dtype=td, device=dev())
+                B.brng_batch_fill(h, B.DIST[dist], code, p0, p1, ob, n)
+                cb = B.brng_get_offset(h)
+            with handle(31, 4, 9) as h:
+                oa = torch.empty(n, dtype=td, device=dev())
+                arrs = [torch.full((n,), p0, dtype=td, device=dev())]
+                if dist != "exponential":
+                    arrs.append(torch.full((n,), p1, dtype=td, device=dev()))
+                sfx = "f32" if dt == np.float32 else "f64"
+                getattr(B, f"brng_{dist}_{sfx}")(h, *arrs, oa, n)
+                assert B.brng_get_offset(h) == cb
+            assert torch.equal(oa, ob), (dist, sfx)
+    with handle(1) as h:
+        with pytest.raises(B.brng.BrngError):
+            B.brng_batch_fill(h, 5, 0, 0.0, 1.0, torch.empty(4, device=dev()), 4)
