@@ -13,13 +13,14 @@
 //   * the parts of Philox that are constant along a chain are hoisted
 //     (17 IMAD.WIDE per block instead of 20; the round-1 product is advanced
 //     with a 64-bit add);
-//   * the chain state is kept SCALED by 2^53: X = x 2^53 = fl(fl(1-y) m) with
-//     m the 53-bit integer of u53 (converted exactly by one I2F.F64.U64 on
-//     the XU pipe), and 1-x = fma(X, -2^-53, 1).  Power-of-two scaling
-//     commutes with IEEE rounding away from under/overflow (values here are
-//     0 or >= 2^-106), so every x, y, sum and fma is bit-identical to the
-//     oracle's unscaled arithmetic while saving the two u53 scalings;
-//   * the histogram bin floor(256 x) = floor(X 2^-45) is read from the bits
+//   * the chain state is kept SCALED by 2^64: X = x 2^64 = fl(fl(1-y) u53 2^64)
+//     where u53 2^64 is the Philox word pair with its low 11 bits cleared,
+//     converted exactly by one I2F.F64.U64 (XU pipe), and 1-x =
+//     fma(X, -2^-64, 1).  Power-of-two scaling commutes with IEEE rounding
+//     away from under/overflow (values here are 0 or >= 2^-106 unscaled), so
+//     every x, y, sum and fma is bit-identical to the oracle's unscaled
+//     arithmetic while saving the two u53 scalings and their shifts;
+//   * the histogram bin floor(256 x) = floor(X 2^-56) is read from the bits
 //     of X with integer ops (ALU pipe), not fp64;
 //   * each thread runs two chains interleaved (ILP) with the round keys in
 //     the kernel-parameter constant bank.
@@ -47,9 +48,9 @@ constexpr int kUnroll = BRNG_GIBBS_UNROLL;                // sweeps per loop ite
 constexpr int kHdr = 16;
 constexpr int kTot = kHdr + 256;
 constexpr int kWarps = kThreads / 32;
-constexpr double kTwo53 = 9007199254740992.0;             // 2^53
-constexpr double kTwoM53 = 1.1102230246251565404e-16;     // 2^-53
-constexpr double kTwoM106 = kTwoM53 * kTwoM53;            // 2^-106
+constexpr double kScale = 18446744073709551616.0;          // 2^64 (state scale)
+constexpr double kInvScale = 5.42101086242752217004e-20;   // 2^-64
+constexpr double kInvScale2 = kInvScale * kInvScale;       // 2^-128
 
 struct GibbsArgs {
   uint64_t n_chains, base, stream_id;
@@ -66,18 +67,20 @@ struct GibbsArgs {
   unsigned long long* err;
 };
 
-// m = the 53-bit integer of u53(lo, hi) as an exact double (u53 = m 2^-53).
-__device__ __forceinline__ double m53(uint32_t lo, uint32_t hi) {
-  return __ull2double_rn((((uint64_t)hi << 32) | lo) >> 11);
+// u53(lo, hi) * 2^64 = m * 2^11 with m = (hi:lo) >> 11: clearing the low 11
+// bits of the 64-bit word gives a value with <= 53 significant bits, so one
+// I2F.F64.U64 converts it exactly (one LOP3, no shifts).
+__device__ __forceinline__ double u53_scaled(uint32_t lo, uint32_t hi) {
+  return __ull2double_rn(((uint64_t)hi << 32) | (lo & 0xFFFFF800u));
 }
 
-// floor(256 x) = floor(X 2^-45) for X = x 2^53 in [0, 2^53): with E the
-// unbiased exponent of X, the bin is the top E-44 bits of 1.mantissa, all in
-// the high word; E < 45 (and X = 0) shift everything out (shift >= 21; PTX
+// floor(256 x) = floor(X 2^-56) for X = x 2^64 in [0, 2^64): with E the
+// unbiased exponent of X, the bin is the top E-55 bits of 1.mantissa, all in
+// the high word; E < 56 (and X = 0) shift everything out (shift >= 21; PTX
 // shr clamps shifts >= 32 to a zero result).
 __device__ __forceinline__ uint32_t bin256_scaled(double X) {
   const uint32_t h = (uint32_t)__double2hiint(X);
-  const uint32_t sh = 1088u - (h >> 20);                    // 20 - (E - 45)
+  const uint32_t sh = 1099u - (h >> 20);                    // 20 - (E - 56)
   uint32_t b;
   asm("shr.b32 %0, %1, %2;" : "=r"(b) : "r"((h & 0xFFFFFu) | 0x100000u), "r"(sh));
   return b;
@@ -149,8 +152,8 @@ __device__ __forceinline__ uint4 chain_block(const ChainKey& ck, uint64_t p0, co
   return c;
 }
 
-// Per-chain state, scaled: X = x 2^53, Y = y 2^53, S1* = s1 2^53,
-// S2*, SXY = s2 2^106.
+// Per-chain state, scaled: X = x 2^64, Y = y 2^64, S1* = s1 2^64,
+// S2*, SXY = s2 2^128.
 struct Chain {
   double X, Y, S1X, S2X, S1Y, S2Y, SXY;
   uint64_t c;
@@ -178,12 +181,12 @@ __device__ __forceinline__ void sweeps(const GibbsArgs& a, const RoundKeys& rk, 
       for (int k = 0; k < CPT; ++k) {
         Chain& q = ch[k];
         const uint4 w = chain_block(ck[k], p0, rk);
-        // x = fl(fl(1-y) u53)  <=>  X = fl(fl(1-y) m),  1-y = fma(Y, -2^-53, 1)
-        q.X = __dmul_rn(__fma_rn(q.Y, -kTwoM53, 1.0), m53(w.x, w.y));
-        q.Y = __dmul_rn(__fma_rn(q.X, -kTwoM53, 1.0), m53(w.z, w.w));
+        // x = fl(fl(1-y) u53)  <=>  X = fl(fl(1-y) u53 2^64),  1-y = fma(Y, -2^-64, 1)
+        q.X = __dmul_rn(__fma_rn(q.Y, -kInvScale, 1.0), u53_scaled(w.x, w.y));
+        q.Y = __dmul_rn(__fma_rn(q.X, -kInvScale, 1.0), u53_scaled(w.z, w.w));
         if (STORE && q.live) {
-          if (a.out_x) a.out_x[(uint64_t)s * a.n_chains + q.c] = __dmul_rn(q.X, kTwoM53);
-          if (a.out_y) a.out_y[(uint64_t)s * a.n_chains + q.c] = __dmul_rn(q.Y, kTwoM53);
+          if (a.out_x) a.out_x[(uint64_t)s * a.n_chains + q.c] = __dmul_rn(q.X, kInvScale);
+          if (a.out_y) a.out_y[(uint64_t)s * a.n_chains + q.c] = __dmul_rn(q.Y, kInvScale);
         }
         if (STATS) {
           q.S1X = __dadd_rn(q.S1X, q.X); q.S2X = __fma_rn(q.X, q.X, q.S2X);
@@ -242,8 +245,8 @@ gibbs_kernel(GibbsArgs a) {
       const bool valid = (y >= 0.0) && (y <= 1.0);
       q.live = real && valid;
       nbad += (real && !valid);
-      q.X = __dmul_rn(x, kTwo53);
-      q.Y = __dmul_rn(valid ? y : qnan, kTwo53);
+      q.X = __dmul_rn(x, kScale);
+      q.Y = __dmul_rn(valid ? y : qnan, kScale);
       q.S1X = q.S2X = q.S1Y = q.S2Y = q.SXY = 0.0;
     }
     sweeps<STORE, false, CPT>(a, rk, 0, a.burn_in, ch, hist_base);
@@ -254,14 +257,14 @@ gibbs_kernel(GibbsArgs a) {
     for (int k = 0; k < CPT; ++k) {
       const Chain& q = ch[k];
       if (q.c >= a.n_chains) continue;
-      const double s1x = __dmul_rn(q.S1X, kTwoM53), s1y = __dmul_rn(q.S1Y, kTwoM53);
-      const double s2x = __dmul_rn(q.S2X, kTwoM106), s2y = __dmul_rn(q.S2Y, kTwoM106);
-      const double sxy = __dmul_rn(q.SXY, kTwoM106);
+      const double s1x = __dmul_rn(q.S1X, kInvScale), s1y = __dmul_rn(q.S1Y, kInvScale);
+      const double s2x = __dmul_rn(q.S2X, kInvScale2), s2y = __dmul_rn(q.S2Y, kInvScale2);
+      const double sxy = __dmul_rn(q.SXY, kInvScale2);
       const double mx = __ddiv_rn(s1x, n), my = __ddiv_rn(s1y, n);
       const double vx = __ddiv_rn(__dsub_rn(s2x, __dmul_rn(s1x, mx)), nm1);
       const double vy = __ddiv_rn(__dsub_rn(s2y, __dmul_rn(s1y, my)), nm1);
       const double cxy = __ddiv_rn(__dsub_rn(sxy, __dmul_rn(s1x, my)), nm1);
-      const double fx = __dmul_rn(q.X, kTwoM53), fy = __dmul_rn(q.Y, kTwoM53);
+      const double fx = __dmul_rn(q.X, kInvScale), fy = __dmul_rn(q.Y, kInvScale);
       if (a.chain_stats) {
         a.chain_stats[0 * a.n_chains + q.c] = mx;
         a.chain_stats[1 * a.n_chains + q.c] = vx;
