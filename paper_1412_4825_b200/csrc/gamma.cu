@@ -42,9 +42,19 @@ __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000
 // decisions are those of the binary64 contract while the two binary64
 // logarithms (and the warp divergence of a squeeze-miss path) disappear from
 // >99.9% of trials.
-__device__ __forceinline__ bool mt_trial(uint4 w, double d, double c, double& g) {
+// d, c are derived from alpha here, after the Philox block and z, so that the
+// parameter load issued when a lane picked its sample overlaps that work.
+__device__ __forceinline__ void mt_consts(double alpha, double& d, double& c) {
+  const double ap = alpha < 1.0 ? alpha + 1.0 : alpha;
+  d = ap - 1.0 / 3.0;
+  c = rsqrt(9.0 * d);                                // 1/sqrt(9d) to ~1 ulp
+}
+
+__device__ __forceinline__ bool mt_trial(uint4 w, double alpha, double& d, double& g) {
   const double L = log(1.0 - u53(w.x, w.y));
   const double z = __dmul_rn(sqrt(-2.0 * L), cospi(2.0 * u32d(w.z)));
+  double c;
+  mt_consts(alpha, d, c);
   const double cz = __dmul_rn(c, z);
   const double t = __dadd_rn(1.0, cz);
   if (!(t > 0.0)) return false;
@@ -92,16 +102,13 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
   uint64_t head = beg + 32;
   uint64_t i = beg + lane;
   bool active = i < end;
-  double alpha = 1.0, beta = 1.0, d = 0.0, c = 0.0;
-  bool valid = false;
+  double alpha = 1.0, beta = 1.0, d = 0.0;
   uint32_t t = 1;
   uint32_t qn = 0;                                   // queued boosts (warp-uniform)
+  // issue the parameter loads only; they are consumed after the next trial's
+  // Philox block and Box-Muller normal
   auto setup = [&]() {
     load(i, alpha, beta);
-    valid = isfinite(alpha) && isfinite(beta) && alpha > 0.0 && beta > 0.0;
-    const double ap = alpha < 1.0 ? alpha + 1.0 : alpha;
-    d = ap - 1.0 / 3.0;
-    c = rsqrt(9.0 * d);                              // 1/sqrt(9d) to ~1 ulp
     t = 1;
   };
   // lanes [0, n) take the last n queue entries, boost and sink them
@@ -122,15 +129,15 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
     bool done = false, boost = false;
     double g = 0.0;
     if (active) {
+      const uint4 w = philox_block(base + (uint64_t)kStride * i + t, stream, k0, k1);
+      const bool valid = isfinite(alpha) && isfinite(beta) && alpha > 0.0 && beta > 0.0;
+      const bool acc = mt_trial(w, alpha, d, g);
       if (!valid) {
         done = true; t = 0; ++nbad;
-      } else {
-        const uint4 w = philox_block(base + (uint64_t)kStride * i + t, stream, k0, k1);
-        if (mt_trial(w, d, c, g)) {
-          done = true;
-        } else if (++t > kMaxTrial) {
-          done = true; t = 0; ++nbad;
-        }
+      } else if (acc) {
+        done = true;
+      } else if (++t > kMaxTrial) {
+        done = true; t = 0; ++nbad;
       }
       boost = done && t != 0 && alpha < 1.0;
       if (done && !boost) sink(i, t != 0 ? g * beta : qnan(), t);
