@@ -174,7 +174,10 @@ struct GammaArgs {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 3) gamma_kernel(GammaArgs<T> a) {
+#ifndef BRNG_GAMMA_MINB
+#define BRNG_GAMMA_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(GammaArgs<T> a) {
   __shared__ BoostItem qs[kThreads / 32][kBoostCap];
   BoostItem* q = qs[threadIdx.x >> 5];
   const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
