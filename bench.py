@@ -480,56 +480,65 @@ def _cores():
 
 def oracle_sample_rates(budget_s=15.0, threads=None):
     """Time the oracle, as it stands, on bounded samples of each config with
-    `threads` workers on disjoint slices.  Returns (rates samples/s per config,
-    description, threads)."""
+    `threads` workers on disjoint slices (ctypes releases the GIL), each
+    sample sized from a short probe so that it takes ~budget_s/5 of wall time.
+    Returns (rates samples/s per config, description, threads)."""
     import numpy as np
     import oracle
     import workloads as W
     P = threads or _cores()
-    scale = max(0.05, budget_s / 15.0)
+    per_cfg = max(0.05, budget_s / 5.0)
     rates, desc = {}, []
 
-    def timed(name, n_units, samples_per_unit, fn, chunk):
-        sl = [(lo, min(lo + chunk, n_units)) for lo in range(0, n_units, chunk)]
-        t = time.perf_counter()
-        oracle.run_parallel(fn, sl, P)
-        dt = time.perf_counter() - t
-        rates[name] = n_units * samples_per_unit / dt
-        desc.append(f"{name}: {n_units} units in {dt:.2f}s")
+    def measure(name, samples_per_unit, n_probe, n_cap, make, chunk):
+        def run(n_units):
+            fn = make(n_units)
+            sl = [(lo, min(lo + chunk, n_units)) for lo in range(0, n_units, chunk)]
+            t = time.perf_counter()
+            oracle.run_parallel(fn, sl, P)
+            return time.perf_counter() - t
+        dt = run(n_probe)
+        n = int(min(n_cap, max(n_probe, n_probe * per_cfg / max(dt, 1e-6))))
+        dt = run(n)
+        rates[name] = n * samples_per_unit / dt
+        desc.append(f"{name}: {n} units in {dt:.2f}s")
 
-    # cfg2: Gaussian and uniform f32 on the cfg2 parameter recipe
-    n2 = int(2**22 * scale * P / 8) // 4 * 4 or 4
-    p2 = {k: v.numpy() for k, v in W.cfg2_params(n2, seed=7).items()}
-    out = np.empty(n2, np.float32)
-    timed("cfg2_gaussian", n2, 1, lambda lo, hi: oracle.lib().orc_gaussian_f32(
-        7, 0, 0, p2["mu"][lo:].ctypes.data, p2["sigma"][lo:].ctypes.data, out[lo:].ctypes.data,
-        lo, hi - lo), 1 << 16)
-    timed("cfg2_uniform", n2, 1, lambda lo, hi: oracle.lib().orc_uniform_f32(
-        7, 0, 0, p2["a"][lo:].ctypes.data, p2["b"][lo:].ctypes.data, out[lo:].ctypes.data,
-        lo, hi - lo), 1 << 16)
-    # cfg3
-    n3 = int(2**20 * scale * P / 8) or 1
-    p3 = {k: v.numpy() for k, v in W.cfg3_params(n3, seed=11).items()}
-    o3 = np.empty(n3); t3 = np.empty(n3, np.uint8)
-    timed("cfg3_gamma", n3, 1, lambda lo, hi: oracle.lib().orc_gamma_f64(
-        11, 0, 0, p3["alpha"][lo:].ctypes.data, p3["beta"][lo:].ctypes.data, o3[lo:].ctypes.data,
-        t3[lo:].ctypes.data, lo, hi - lo), 1 << 14)
-    # cfg4
-    D = int(2000 * scale * P / 8) or 1
-    a4 = W.cfg4_params(D, 256, seed=3).numpy()
-    o4 = np.empty_like(a4); t4 = np.empty(a4.shape, np.uint8)
-    scratch = [np.empty(256) for _ in range(D)]
-    timed("cfg4_dirichlet", D, 256, lambda lo, hi: oracle.lib().orc_dirichlet_f32(
-        3, 0, 0, a4[lo:].ctypes.data, 256, o4[lo:].ctypes.data, t4[lo:].ctypes.data, lo, hi - lo,
-        scratch[lo].ctypes.data), 64)
-    # cfg5 (and cfg1's per-sweep cost): a stride subset of the 2^24 chains
-    nc = int(2**11 * scale * P / 8) or 1
-    st = np.empty((5, nc)); fx = np.empty((2, nc)); tot = np.zeros((nc, 272))
+    def cfg2(kind):
+        def make(n):
+            n = max(4, n // 4 * 4)
+            p2 = {k: v.numpy() for k, v in W.cfg2_params(n, seed=7).items()}
+            out = np.empty(n, np.float32)
+            f = oracle.lib().orc_gaussian_f32 if kind == "g" else oracle.lib().orc_uniform_f32
+            k0, k1 = ("mu", "sigma") if kind == "g" else ("a", "b")
+            return lambda lo, hi: f(7, 0, 0, p2[k0][lo:].ctypes.data, p2[k1][lo:].ctypes.data,
+                                    out[lo:].ctypes.data, lo, hi - lo)
+        return make
+    measure("cfg2_gaussian", 1, 1 << 18, 1 << 27, cfg2("g"), 1 << 16)
+    measure("cfg2_uniform", 1, 1 << 18, 1 << 27, cfg2("u"), 1 << 16)
 
-    def gib(lo, hi):
-        oracle.lib().orc_gibbs_triangle(42, lo, 0, hi - lo, 4096, None, None, 0, None, None,
-                                        None, None, tot[lo].ctypes.data)
-    timed("cfg5_gibbs", nc, 2 * 4096, gib, 16)
+    def cfg3(n):
+        p3 = {k: v.numpy() for k, v in W.cfg3_params(n, seed=11).items()}
+        o3 = np.empty(n); t3 = np.empty(n, np.uint8)
+        return lambda lo, hi: oracle.lib().orc_gamma_f64(
+            11, 0, 0, p3["alpha"][lo:].ctypes.data, p3["beta"][lo:].ctypes.data,
+            o3[lo:].ctypes.data, t3[lo:].ctypes.data, lo, hi - lo)
+    measure("cfg3_gamma", 1, 1 << 16, 1 << 26, cfg3, 1 << 14)
+
+    def cfg4(D):
+        a4 = W.cfg4_params(D, 256, seed=3).numpy()
+        o4 = np.empty_like(a4); t4 = np.empty(a4.shape, np.uint8)
+        scratch = np.empty((D, 256))
+        return lambda lo, hi: oracle.lib().orc_dirichlet_f32(
+            3, 0, 0, a4[lo:].ctypes.data, 256, o4[lo:].ctypes.data, t4[lo:].ctypes.data, lo,
+            hi - lo, scratch[lo].ctypes.data)
+    measure("cfg4_dirichlet", 256, 256, 200_000, cfg4, 64)
+
+    def cfg5(nc):
+        tot = np.zeros((nc, 272))
+        return lambda lo, hi: oracle.lib().orc_gibbs_triangle(
+            42, lo, 0, hi - lo, 4096, None, None, 0, None, None, None, None, tot[lo].ctypes.data)
+    # a contiguous subset of cfg5's 2^24 chains, full 4096 sweeps each
+    measure("cfg5_gibbs", 2 * 4096, 256, 1 << 20, cfg5, 16)
     rates["cfg1_gibbs"] = rates["cfg5_gibbs"]
     return rates, "; ".join(desc), P
 

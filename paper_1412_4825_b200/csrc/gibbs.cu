@@ -47,7 +47,6 @@ constexpr int kCPT = BRNG_GIBBS_CPT;                      // chains per thread
 constexpr int kUnroll = BRNG_GIBBS_UNROLL;                // sweeps per loop iteration
 constexpr int kHdr = 16;
 constexpr int kTot = kHdr + 256;
-constexpr int kWarps = kThreads / 32;
 constexpr double kScale = 18446744073709551616.0;          // 2^64 (state scale)
 constexpr double kInvScale = 5.42101086242752217004e-20;   // 2^-64
 constexpr double kInvScale2 = kInvScale * kInvScale;       // 2^-128
