@@ -29,53 +29,11 @@ constexpr uint32_t kFull = 0xffffffffu;
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
-// One Marsaglia-Tsang trial from one Philox block (contract R-09).
-//   z = sqrt(-2 ln(1-u53(w0,w1))) cos(2 pi u32d(w2)),  U = 1 - u32d(w3)
-//   t = 1 + c z (reject if t <= 0), v = t^3, accept iff
-//   ln U < z^2/2 + d - d v + d ln v,  g = d v.
-// The value g needs binary64; the DECISION is taken from a binary32
-// evaluation of the cancellation-free form
-//   rhs = z^2/2 + d (log1p(wv) - wv),  wv = v - 1 = cz (3 + cz (3 + cz)),
-// whose absolute error is < 1e-6 (1 + z^2/2 + d|wv| + |ln U|) (log1pf/logf
-// are ~1 ulp).  Only when the binary32 margin lies inside a band 10x wider is
-// the exact binary64 test evaluated, in the oracle's operation order -- so the
-// decisions are those of the binary64 contract while the two binary64
-// logarithms (and the warp divergence of a squeeze-miss path) disappear from
-// >99.9% of trials.
-// d, c are derived from alpha here, after the Philox block and z, so that the
-// parameter load issued when a lane picked its sample overlaps that work.
-__device__ __forceinline__ void mt_consts(double alpha, double& d, double& c) {
-  const double ap = alpha < 1.0 ? alpha + 1.0 : alpha;
-  d = ap - 1.0 / 3.0;
-  c = rsqrt(9.0 * d);                                // 1/sqrt(9d) to ~1 ulp
-}
-
-__device__ __forceinline__ bool mt_trial(uint4 w, double alpha, double& d, double& g) {
-  const double L = log(1.0 - u53(w.x, w.y));
-  const double z = __dmul_rn(sqrt(-2.0 * L), cospi(2.0 * u32d(w.z)));
-  double c;
-  mt_consts(alpha, d, c);
-  const double cz = __dmul_rn(c, z);
-  const double t = __dadd_rn(1.0, cz);
-  if (!(t > 0.0)) return false;
-  const double v = __dmul_rn(__dmul_rn(t, t), t);
-  g = __dmul_rn(d, v);
-  const double U = 1.0 - u32d(w.w);
-  const double wv = cz * (3.0 + cz * (3.0 + cz));
-  const float wf = (float)wv;
-  const float lf = log1pf(wf) - wf;
-  const float lnu = logf((float)U);
-  const double z2h = 0.5 * z * z;
-  const double m = fma(d, (double)lf, z2h) - (double)lnu;
-  const double band = 1e-5 * (1.0 + z2h + d * fabs(wv) + fabs((double)lnu));
-  if (m > band) return true;
-  if (m < -band) return false;
-  // rare: the exact binary64 test, operation order of the contract/oracle
-  const double rhs = __dadd_rn(__dsub_rn(__dadd_rn(__dmul_rn(__dmul_rn(z, z), 0.5), d),
-                                         __dmul_rn(d, v)),
-                               __dmul_rn(d, log(v)));
-  return log(U) < rhs;
-}
+// One Marsaglia-Tsang trial (R-09) and the alpha<1 boost (R-10): the public
+// device API's (include/brng_device.cuh): binary32 decision with a binary64
+// recheck band, binary64 values.
+using brng_dev::mt_boost;
+using brng_dev::mt_trial;
 
 // alpha<1 boost work item, parked in a per-warp shared-memory queue so that
 // boosts run as full warps instead of as a divergent branch (36% of cfg3's
@@ -118,7 +76,7 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
       const BoostItem it = q[qn - n + lane];
       const uint64_t ii = it.i_t & 0x00FFFFFFFFFFFFFFull;
       const uint4 wb = philox_block(base + (uint64_t)kStride * ii, stream, k0, k1);
-      const double gb = it.g * exp(log(1.0 - u53(wb.x, wb.y)) / it.alpha);
+      const double gb = mt_boost(wb, it.g, it.alpha);
       sink(ii, gb * it.beta, (uint32_t)(it.i_t >> 56));
     }
     qn -= n;

@@ -1,0 +1,82 @@
+// A "user" translation unit that draws its deviates through the public device
+// API (include/brng_device.cuh) one sample at a time -- the paper's
+// one-at-a-time getters called inside the consumer's own loop.  Used by
+// tests/test_gpu_device_api.py to check the getters against the bulk C ABI.
+#include <brng_device.cuh>
+
+namespace {
+__global__ void k_fill(int dist, uint64_t seed, uint64_t stream, uint64_t base, const double* p0,
+                       const double* p1, double* out, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const brng_dev::Key k = brng_dev::make_key(seed);
+  double v = 0.0;
+  switch (dist) {
+    case 2: v = brng_dev::uniform_f64(k, stream, base, i, p0[i], p1[i]); break;
+    case 3: v = brng_dev::gaussian_f64(k, stream, base, i, p0[i], p1[i]); break;
+    case 4: v = brng_dev::exponential_f64(k, stream, base, i, p0[i]); break;
+    case 5: v = brng_dev::log_uniform_f64(k, stream, base, i); break;
+    case 6: v = brng_dev::laplace_f64(k, stream, base, i, p0[i], p1[i]); break;
+    case 7: v = brng_dev::weibull_f64(k, stream, base, i, p0[i], p1[i]); break;
+  }
+  out[i] = v;
+}
+__global__ void k_fill32(int dist, uint64_t seed, uint64_t stream, uint64_t base, const float* p0,
+                         const float* p1, float* out, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const brng_dev::Key k = brng_dev::make_key(seed);
+  float v = 0.0f;
+  switch (dist) {
+    case 2: v = brng_dev::uniform_f32(k, stream, base, i, p0[i], p1[i]); break;
+    case 3: v = brng_dev::gaussian_f32(k, stream, base, i, p0[i], p1[i]); break;
+    case 4: v = brng_dev::exponential_f32(k, stream, base, i, p0[i]); break;
+  }
+  out[i] = v;
+}
+__global__ void k_gamma(uint64_t seed, uint64_t stream, uint64_t base, const double* alpha,
+                        const double* beta, double* out, unsigned char* trials, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t t;
+  out[i] = brng_dev::gamma_f64(brng_dev::make_key(seed), stream, base, i, alpha[i], beta[i], &t);
+  trials[i] = (unsigned char)t;
+}
+// Fig. 1 of the paper as a user kernel: one chain per thread.
+__global__ void k_gibbs(uint64_t seed, uint64_t stream_id, uint64_t base, uint64_t n_chains,
+                        uint64_t n_sweeps, double* out_x, double* out_y) {
+  const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_chains) return;
+  const brng_dev::Key k = brng_dev::make_key(seed);
+  double x = 0.5, y = 0.5;
+  for (uint64_t s = 0; s < n_sweeps; ++s) {
+    brng_dev::gibbs_sweep(k, stream_id + c, base + s, x, y);
+    out_x[s * n_chains + c] = x;
+    out_y[s * n_chains + c] = y;
+  }
+}
+unsigned grid(uint64_t n) { return (unsigned)((n + 255) / 256); }
+}  // namespace
+
+extern "C" {
+int dev_fill(int dist, uint64_t seed, uint64_t stream, uint64_t base, const double* p0,
+             const double* p1, double* out, uint64_t n, void* s) {
+  k_fill<<<grid(n), 256, 0, (cudaStream_t)s>>>(dist, seed, stream, base, p0, p1, out, n);
+  return (int)cudaGetLastError();
+}
+int dev_fill32(int dist, uint64_t seed, uint64_t stream, uint64_t base, const float* p0,
+               const float* p1, float* out, uint64_t n, void* s) {
+  k_fill32<<<grid(n), 256, 0, (cudaStream_t)s>>>(dist, seed, stream, base, p0, p1, out, n);
+  return (int)cudaGetLastError();
+}
+int dev_gamma(uint64_t seed, uint64_t stream, uint64_t base, const double* a, const double* b,
+              double* out, unsigned char* tr, uint64_t n, void* s) {
+  k_gamma<<<grid(n), 256, 0, (cudaStream_t)s>>>(seed, stream, base, a, b, out, tr, n);
+  return (int)cudaGetLastError();
+}
+int dev_gibbs(uint64_t seed, uint64_t stream_id, uint64_t base, uint64_t nc, uint64_t ns,
+              double* ox, double* oy, void* s) {
+  k_gibbs<<<grid(nc), 256, 0, (cudaStream_t)s>>>(seed, stream_id, base, nc, ns, ox, oy);
+  return (int)cudaGetLastError();
+}
+}
