@@ -166,8 +166,15 @@ __device__ __forceinline__ void std_block(uint4 w, double* s) {
 }
 
 // ---- kernels ------------------------------------------------------------------
+#ifndef BRNG_FILL_BPT
+#define BRNG_FILL_BPT 2
+#endif
+constexpr int kBPT = BRNG_FILL_BPT;    // Philox blocks per thread per iteration
+
 // SCALAR: every sample uses the fixed parameters (s0, s1) -- the fixed-
 // parameter "Batch" scenario of the paper's Fig. 2, 4 B/sample.
+// Each thread handles kBPT blocks per iteration (stride apart): all parameter
+// loads are issued before any Philox work, for memory-level parallelism.
 template <typename T, int DIST, bool SCALAR = false>
 __global__ void __launch_bounds__(kThreads) fill_kernel(FillArgs<T> a) {
   constexpr int S = spb<T, DIST>();
@@ -175,28 +182,44 @@ __global__ void __launch_bounds__(kThreads) fill_kernel(FillArgs<T> a) {
   const uint64_t nblk = (a.n + S - 1) / S;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   uint32_t bad = 0;
-  for (uint64_t j = (uint64_t)blockIdx.x * kThreads + threadIdx.x; j < nblk; j += stride) {
-    const uint4 w = philox_block(a.base + j, a.stream, a.k0, a.k1);
-    T s[S];
-    std_block<DIST>(w, s);
-    const uint64_t i0 = j * S;
-    T p0[S], p1[S], o[S];
-    if (a.vec && i0 + S <= a.n) {
-      if (NP >= 1) Vec<T, S>::ld(a.p0 + i0, p0);
-      if (NP >= 2) Vec<T, S>::ld(a.p1 + i0, p1);
+  for (uint64_t j0 = (uint64_t)blockIdx.x * kThreads + threadIdx.x; j0 < nblk;
+       j0 += kBPT * stride) {
+    T p0[kBPT][S], p1[kBPT][S];
+    bool full[kBPT];
 #pragma unroll
-      for (int k = 0; k < S; ++k)
-        o[k] = SCALAR ? xform<DIST>(a.s0, a.s1, s[k], bad)
-                      : xform<DIST>(NP >= 1 ? p0[k] : T(0), NP >= 2 ? p1[k] : T(0), s[k], bad);
-      Vec<T, S>::st(a.out + i0, o);
-    } else {
+    for (int b = 0; b < kBPT; ++b) {
+      const uint64_t j = j0 + b * stride;
+      full[b] = a.vec && (j + 1) * S <= a.n;
+      if (full[b]) {
+        if (NP >= 1) Vec<T, S>::ld(a.p0 + j * S, p0[b]);
+        if (NP >= 2) Vec<T, S>::ld(a.p1 + j * S, p1[b]);
+      }
+    }
 #pragma unroll
-      for (int k = 0; k < S; ++k) {
-        const uint64_t i = i0 + k;
-        if (i < a.n) {
-          const T q0 = SCALAR ? a.s0 : (NP >= 1 ? a.p0[i] : T(0));
-          const T q1 = SCALAR ? a.s1 : (NP >= 2 ? a.p1[i] : T(0));
-          a.out[i] = xform<DIST>(q0, q1, s[k], bad);
+    for (int b = 0; b < kBPT; ++b) {
+      const uint64_t j = j0 + b * stride;
+      if (j >= nblk) break;
+      const uint4 w = philox_block(a.base + j, a.stream, a.k0, a.k1);
+      T s[S];
+      std_block<DIST>(w, s);
+      const uint64_t i0 = j * S;
+      if (full[b]) {
+        T o[S];
+#pragma unroll
+        for (int k = 0; k < S; ++k)
+          o[k] = SCALAR ? xform<DIST>(a.s0, a.s1, s[k], bad)
+                        : xform<DIST>(NP >= 1 ? p0[b][k] : T(0), NP >= 2 ? p1[b][k] : T(0), s[k],
+                                      bad);
+        Vec<T, S>::st(a.out + i0, o);
+      } else {
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+          const uint64_t i = i0 + k;
+          if (i < a.n) {
+            const T q0 = SCALAR ? a.s0 : (NP >= 1 ? a.p0[i] : T(0));
+            const T q1 = SCALAR ? a.s1 : (NP >= 2 ? a.p1[i] : T(0));
+            a.out[i] = xform<DIST>(q0, q1, s[k], bad);
+          }
         }
       }
     }
@@ -225,7 +248,7 @@ inline bool aligned(const void* p, uintptr_t bytes) {
 }
 
 inline unsigned grid_for(uint64_t nblk, const Ctx& ctx) {
-  const uint64_t want = (nblk + kThreads - 1) / kThreads;
+  const uint64_t want = (nblk + (uint64_t)kThreads * kBPT - 1) / ((uint64_t)kThreads * kBPT);
   const uint64_t cap = (uint64_t)ctx.num_sms * 8 * 4;  // 8 CTAs/SM resident x 4 waves
   return (unsigned)(want < cap ? (want ? want : 1) : cap);
 }

@@ -1,6 +1,6 @@
 """Time build variants of libbrng (tools/variants/*.so) on one kernel.
 
-usage: python tools/variant_time.py gibbs|gamma|dirichlet [lib ...]
+usage: python tools/variant_time.py gibbs|gamma|dirichlet|gaussian|uniform [lib ...]
 Each variant runs in its own process (BRNG_LIB=...); prints ms and a hash of
 the outputs so variants can be checked for identical results.
 """
@@ -39,6 +39,17 @@ elif what == "gamma":
     def run():
         B.brng_set_offset(h, 0)
         B.brng_gamma_f64(h, p["alpha"], p["beta"], o, n, None)
+    outs = [o]
+elif what in ("gaussian", "uniform"):
+    n = 1 << 28
+    p = W.cfg2_params(n, seed=7, device=dev)
+    o = torch.empty(n, device=dev)
+    h = B.brng_create(7, 0); B.brng_set_cuda_stream(h, s)
+    k0, k1 = ("mu", "sigma") if what == "gaussian" else ("a", "b")
+    fn = getattr(B, f"brng_{what}_f32")
+    def run():
+        B.brng_set_offset(h, 0)
+        fn(h, p[k0], p[k1], o, n)
     outs = [o]
 else:
     D, K = 1000000, 256
