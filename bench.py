@@ -234,9 +234,18 @@ def gpu_arm(args):
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    # plumbing check only (tests/tools): BRNG_BENCH_DEVICE pins every rank to
+    # one GPU and BRNG_BENCH_BACKEND=gloo replaces NCCL, so the N>1 code path
+    # runs on a 1-GPU box (independent processes, nothing waits on a peer
+    # kernel); numbers from such a run are not bench values
+    local = int(os.environ.get("BRNG_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BRNG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_1412_4825_b200 as B
 
     hbm_peak, sm_max_cfg, peak_kind = load_peaks()
