@@ -45,6 +45,10 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kCPT = BRNG_GIBBS_CPT;                      // chains per thread
 constexpr int kUnroll = BRNG_GIBBS_UNROLL;                // sweeps per loop iteration
+#ifndef BRNG_GIBBS_SMALL_UNROLL
+#define BRNG_GIBBS_SMALL_UNROLL 2
+#endif
+constexpr int kSmallUnroll = BRNG_GIBBS_SMALL_UNROLL;     // small (1 chain/thread) launches
 constexpr int kHdr = 16;
 constexpr int kTot = kHdr + 256;
 constexpr double kScale = 18446744073709551616.0;          // 2^64 (state scale)
@@ -160,7 +164,7 @@ struct Chain {
 };
 
 // Sweeps [s_begin, s_end) of the thread's kCPT chains.
-template <bool STORE, bool STATS, int CPT>
+template <bool STORE, bool STATS, int CPT, int UNROLL>
 __device__ __forceinline__ void sweeps(const GibbsArgs& a, const RoundKeys& rk, uint32_t s_begin,
                                        uint32_t s_end, Chain (&ch)[CPT], uint32_t hist_base) {
   uint32_t s = s_begin;
@@ -174,7 +178,7 @@ __device__ __forceinline__ void sweeps(const GibbsArgs& a, const RoundKeys& rk, 
     for (int k = 0; k < CPT; ++k)
       ck[k] = chain_key(a.stream_id + ch[k].c, (uint32_t)(pos >> 32), a);
     uint64_t p0 = (uint64_t)kPhiloxM0 * pos_lo;
-#pragma unroll kUnroll
+#pragma unroll UNROLL
     for (; s < e; ++s) {
 #pragma unroll
       for (int k = 0; k < CPT; ++k) {
@@ -248,8 +252,11 @@ gibbs_kernel(GibbsArgs a) {
       q.Y = __dmul_rn(valid ? y : qnan, kScale);
       q.S1X = q.S2X = q.S1Y = q.S2Y = q.SXY = 0.0;
     }
-    sweeps<STORE, false, CPT>(a, rk, 0, a.burn_in, ch, hist_base);
-    sweeps<STORE, true, CPT>(a, rk, a.burn_in, a.n_sweeps, ch, hist_base);
+    // one chain per thread (latency-bound small launches): unroll deeper so
+    // the Philox blocks of several sweeps overlap the serial x/y update chain
+    constexpr int U = CPT == 1 ? kSmallUnroll : kUnroll;
+    sweeps<STORE, false, CPT, U>(a, rk, 0, a.burn_in, ch, hist_base);
+    sweeps<STORE, true, CPT, U>(a, rk, a.burn_in, a.n_sweeps, ch, hist_base);
 
     double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll

@@ -21,7 +21,17 @@ what = WHAT
 dev = torch.device("cuda:0")
 s = torch.cuda.current_stream().cuda_stream
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-if what == "gibbs":
+if what == "gibbs1":
+    nc, ns = 1024, 1000
+    ox = torch.empty(ns, nc, dtype=torch.float64, device=dev)
+    oy = torch.empty_like(ox)
+    tot = torch.empty(B.TOTALS_LEN, dtype=torch.float64, device=dev)
+    h = B.brng_create(42, 0); B.brng_set_cuda_stream(h, s)
+    def run():
+        B.brng_set_offset(h, 0)
+        B.brng_gibbs_triangle(h, nc, ns, None, None, 0, ox, oy, None, None, tot)
+    outs = [ox, oy, tot[16:]]
+elif what == "gibbs":
     nc, ns = 1 << 24, 4096
     st = torch.empty(5, nc, dtype=torch.float64, device=dev)
     fx = torch.empty(2, nc, dtype=torch.float64, device=dev)
