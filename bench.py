@@ -70,6 +70,30 @@ def ncu_traffic(kernel_substr):
     return best
 
 
+NCU_KERNEL = {"cfg1_gibbs": "gibbs_kernel<1, 1, 64>", "cfg2_gaussian": "fill_f32_kernel<3>",
+              "cfg2_uniform": "fill_f32_kernel<2>", "cfg3_gamma": "gamma_kernel<double>",
+              "cfg4_dirichlet": "dirichlet_smem_kernel<float>",
+              "cfg5_gibbs": "gibbs_kernel<0, 2, 256>"}
+
+
+def ncu_evidence(kernel_substr):
+    """Pipe / issue / DRAM utilisation of a kernel from the committed ncu
+    summary (profiles/*_ncu.json), labelled with its file; {} if absent."""
+    import glob
+    ev = {}
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu.json"))):
+        try:
+            with open(path) as f:
+                for k in json.load(f)["kernels"]:
+                    if kernel_substr in k.get("kernel", ""):
+                        ev = {m: k[m] for m in ("issue_active_pct", "fmaheavy_pct", "alu_pct",
+                                                "dram_pct_peak", "warps_active_pct") if m in k}
+                        ev["source"] = os.path.basename(path)
+        except Exception:
+            continue
+    return ev
+
+
 def load_peaks():
     try:
         with open(PEAKS_PATH) as f:
@@ -313,6 +337,9 @@ def gpu_arm(args):
             a = GIBBS_PIPE_OPS_PER_SWEEP * (wl.samples[n] / 2) / t
             d.update(bound="alu", frac=round(a / pipe_peak, 4),
                      Gsweeps_per_s=round(wl.samples[n] / 2 / t / 1e9, 3))
+        ev = ncu_evidence(NCU_KERNEL.get(n, "?"))
+        if ev:
+            d["ncu"] = ev
         bd[n] = d
     dom = max(names, key=lambda n: per[n])
     t_dom = per[dom] * 1e-3
