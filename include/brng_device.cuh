@@ -80,24 +80,170 @@ __device__ __forceinline__ double u53(uint32_t lo, uint32_t hi) {
 }
 __device__ __forceinline__ double u32d(uint32_t w) { return (double)w * 0x1p-32; }
 
+// ---- binary64 math of the Gamma trial and boost ---------------------------------
+// The Gamma path is bound by instruction issue (DESIGN.md §7 K3), and
+// libdevice's log/cospi/exp/sqrt are general-purpose (special-case branches,
+// 60-100 instructions each, double constants rematerialised per use).  These
+// versions cover exactly the arguments the trial produces: lookup tables
+// (brng_device_tables.cuh) plus short Taylor polynomials whose truncation
+// error is < 1e-19, coefficients in the constant bank (DFMA reads them as
+// operands), no special-case branches.  Errors are ~1-2 ulp (tests/
+// test_gpu_device_api.py pins them against mpmath), far inside the 1e-12
+// value tolerance, and relative-accurate where the trial needs it.
+}  // namespace brng_dev
+#include "brng_device_tables.cuh"
+namespace brng_dev {
+namespace dm {
+enum {
+  kL7, kL6, kL5, kL4, kL3, kL2,          // ln: 1/7, -1/6, 1/5, -1/4, 1/3, -1/2
+  kLn2Hi, kLn2Lo, kRndM128, kI2dBias,    // ln 2 split; 1.5*2^52 - 128; 2^52 + 2^31
+  kS7, kS5, kS3, kC6, kC4, kTwoPi32,     // sin/cos Taylor; 2 pi / 2^32
+  kE6, kE5, kE4, kE3, kInvLn2x64, kLn2Hi64, kLn2Lo64, kRnd,
+  kNumConst
+};
+static __constant__ double kC[kNumConst] = {
+    1.0 / 7.0, -1.0 / 6.0, 0.2, -0.25, 1.0 / 3.0, -0.5,
+    0x1.62e42feep-1,                 // 32 significant bits: e * ln2_hi is exact
+    0x1.a39ef35793c76p-33,           // ln 2 - ln2_hi
+    6755399441055744.0 - 128.0, 4503599627370496.0 + 2147483648.0,
+    -1.0 / 5040.0, 1.0 / 120.0, -1.0 / 6.0, -1.0 / 720.0, 1.0 / 24.0,
+    0x1.921fb54442d18p-30,           // 2 pi / 2^32
+    1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0,
+    0x1.71547652b82fep+6,            // 64 / ln 2
+    0x1.62e42feep-7, 0x1.a39ef35793c76p-39,   // ln2_hi / 64, ln2_lo / 64
+    6755399441055744.0,              // 1.5 * 2^52: round-to-integer shifter
+};
+// exact binary64 of a 32-bit signed integer without the I2F pipe
+__device__ __forceinline__ double i2d(int v) {
+  return __hiloint2double(0x43300000, v ^ (int)0x80000000) - kC[kI2dBias];
+}
+// 1 - u53(lo, hi), exactly, from the bits: with k = (hi:lo) >> 11 (53 bits),
+// D = 2^52 + (k mod 2^52) and t = bit 52 of k, 1 - k 2^-53 = (t ? 1 : 1.5) -
+// D 2^-53 (one exact FMA; no integer->double conversion).
+__device__ __forceinline__ double one_minus_u53(uint32_t lo, uint32_t hi) {
+  const double D = __hiloint2double(0x43300000 | ((hi >> 11) & 0xFFFFF),
+                                    (int)__funnelshift_r(lo, hi, 11));
+  const double C = __hiloint2double(0x3FF80000 ^ ((hi >> 12) & 0x80000), 0);
+  return fma(D, -0x1p-53, C);
+}
+// ln x for a positive normal x.  x = 2^e m, m in [sqrt(1/2), sqrt(2));
+// j = round(128 (m-1)), c_j ~ 1/(1+j/128), r = m c_j - 1 (one rounding, |r| <
+// 0.0056); ln x = e ln2 - ln c_j + log1p(r), log1p by its Taylor series to
+// r^7.  c_0 = 1 and ln c_0 = 0, so for x near 1 the result is log1p(x-1)
+// to ~1 ulp relative.
+__device__ __forceinline__ double ln_pos(double x) {
+  const int hx = __double2hiint(x);
+  const int e = (hx - 0x3FE6A09E) >> 20;
+  const double m = __hiloint2double(hx - e * (1 << 20), __double2loint(x));
+  const int j = __double2loint(fma(m, 128.0, kC[kRndM128]));
+  const double2 ct = __ldg(&tab::kLn[j + tab::kLnOff]);
+  const double r = fma(m, ct.x, -1.0);
+  double q = fma(r, kC[kL7], kC[kL6]);
+  q = fma(r, q, kC[kL5]);
+  q = fma(r, q, kC[kL4]);
+  q = fma(r, q, kC[kL3]);
+  q = fma(r, q, kC[kL2]);
+  const double de = i2d(e);
+  const double lo = fma(r * r, q, de * kC[kLn2Lo]) + r;
+  return fma(de, kC[kLn2Hi], ct.y) + lo;
+}
+// cos(2 pi w 2^-32): j = round(w / 2^24) mod 256, b = 2 pi (w - j 2^24) 2^-32
+// (|b| <= pi/256); cos(a_j + b) = C_j cos b - S_j sin b with Taylor cos b - 1
+// to b^6 and sin b to b^7.  Absolute error ~1e-16.
+__device__ __forceinline__ double cos2pi_u32(uint32_t w) {
+  const uint32_t j = (w + 0x800000u) >> 24;
+  const double b = i2d((int)(w - (j << 24))) * kC[kTwoPi32];
+  const double2 cs = __ldg(&tab::kCos[j]);
+  const double b2 = b * b;
+  const double s = fma(b2 * b, fma(b2, fma(b2, kC[kS7], kC[kS5]), kC[kS3]), b);
+  const double cm1 = b2 * fma(b2, fma(b2, kC[kC6], kC[kC4]), -0.5);
+  return cs.x + fma(cs.x, cm1, -cs.y * s);
+}
+// e^y for finite y <= 0: k = round(64 y / ln 2), r = y - k ln2/64 (|r| <=
+// 0.0055, Cody-Waite), e^y = 2^(k>>6) 2^((k&63)/64) e^r, e^r - 1 by Taylor
+// to r^6.  y < -700 (result near/below the normal range) takes libdevice.
+__device__ __forceinline__ double exp_nonpos(double y) {
+  if (y < -700.0) return exp(y);
+  const double t = fma(y, kC[kInvLn2x64], kC[kRnd]);
+  const int k = __double2loint(t);
+  const double kd = t - kC[kRnd];
+  double r = fma(kd, -kC[kLn2Hi64], y);
+  r = fma(kd, -kC[kLn2Lo64], r);
+  double q = fma(r, kC[kE6], kC[kE5]);
+  q = fma(r, q, kC[kE4]);
+  q = fma(r, q, kC[kE3]);
+  q = fma(r, q, 0.5);
+  const double p = fma(r * r, q, r);
+  const double T = __ldg(&tab::kExp2[k & 63]);
+  const double v = fma(T, p, T);
+  return __hiloint2double(__double2hiint(v) + (k >> 6) * (1 << 20), __double2loint(v));
+}
+// 1/sqrt(x) for a positive normal x: MUFU.RSQ64H seed (~2^-22) and one
+// cubic Newton step y (1 + e/2 + 3e^2/8), e = 1 - x y^2: ~1 ulp.
+__device__ __forceinline__ double rsqrt_pos(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x * y, y, 1.0);
+  return fma(y * e, fma(e, 0.375, 0.5), y);
+}
+// sqrt(x) for x = 0 or a positive normal: x * rsqrt(x) (~2 ulp).
+__device__ __forceinline__ double sqrt_nonneg(double x) {
+  return x > 0.0 ? x * rsqrt_pos(x) : 0.0;
+}
+// ln x in binary32 by MUFU.LG2 (flushes subnormal x to 0 -> -inf).  Error
+// <= 2^-22 ln2 absolute for x in [1/2, 2], else <= 2 ulp of log2 x.
+__device__ __forceinline__ float ln_approx_f32(float x) {
+  float l;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(x));
+  return l * 0.69314718f;
+}
+}  // namespace dm
+
 // ---- Marsaglia-Tsang trial (R-08, R-09) -----------------------------------------
-// d = alpha' - 1/3, c = 1/sqrt(9 d) (rsqrt, ~1 ulp).
+// d = alpha' - 1/3, c = 1/sqrt(9 d) (~1 ulp).
 __device__ __forceinline__ void mt_consts(double alpha, double& d, double& c) {
   const double ap = alpha < 1.0 ? alpha + 1.0 : alpha;
   d = ap - 1.0 / 3.0;
-  c = rsqrt(9.0 * d);
+  c = dm::rsqrt_pos(9.0 * d);
+}
+// The binary32 screen of the acceptance test (see mt_trial): +1 accept,
+// -1 reject, 0 = margin inside the error band (decide with mt_exact).
+__device__ __forceinline__ int mt_screen(double z, double d, double t, uint32_t w3) {
+  const float tf = (float)t, zf = (float)z, df = (float)d;
+  const float z2hf = 0.5f * zf * zf;
+  const float wf = fmaf(tf * tf, tf, -1.0f);
+  const float lnt = dm::ln_approx_f32(tf);
+  const float lnu = dm::ln_approx_f32(fmaf(__uint2float_rn(~w3), 0x1p-32f, 0x1p-32f));
+  const float m = fmaf(df, fmaf(3.0f, lnt, -wf), z2hf) - lnu;
+  const float band =
+      0x1p-17f * (1.0f + z2hf + df * (1.0f + fabsf(wf) + 3.0f * fabsf(lnt)) + fabsf(lnu));
+  return m > band ? 1 : (m < -band ? -1 : 0);
+}
+// The exact binary64 test in the contract's operation order (R-09):
+// ln U < ((z z) 0.5 + d) - d v + d ln v, U = 1 - u32d(w3).
+__device__ __forceinline__ bool mt_exact(double z, double d, double v, uint32_t w3) {
+  const double U = 1.0 - u32d(w3);
+  const double rhs = __dadd_rn(__dsub_rn(__dadd_rn(__dmul_rn(__dmul_rn(z, z), 0.5), d),
+                                         __dmul_rn(d, v)),
+                               __dmul_rn(d, log(v)));
+  return log(U) < rhs;
 }
 // One trial from one Philox block: z = sqrt(-2 ln(1-u53(w0,w1))) cos(2 pi
 // u32d(w2)), U = 1 - u32d(w3); reject if 1+cz <= 0, else v = (1+cz)^3 and
-// accept iff ln U < z^2/2 + d - d v + d ln v; g = d v (binary64).  The
-// decision is evaluated in binary32 on the cancellation-free form
-// z^2/2 + d (log1p(w) - w), w = v - 1, whose error is < 1e-6 (1 + z^2/2 +
-// d|w| + |ln U|); margins inside a 10x band re-run the exact binary64 test in
-// the contract's operation order, so decisions are the binary64 contract's.
+// accept iff ln U < z^2/2 + d - d v + d ln v; g = d v (binary64 values).
+//
+// Decision.  A binary32 screen evaluates the margin on the form
+//   m = z^2/2 + d (3 ln t - w) - ln U,   t = 1 + cz, w = t^3 - 1,
+// (equal to rhs - ln U in exact arithmetic) with MUFU.LG2 logs.  Its error is
+// below 2^-19.4 (1 + z^2/2 + d (1 + |w| + 3|ln t|) + |ln U|) (DESIGN.md §7:
+// lg2.approx 2^-22 absolute on [1/2,2] / 2 ulp elsewhere, 2^-24 per rounding);
+// margins outside 2^-17 times that sum are decided by their sign, the rest
+// (~0.1% of trials) re-run the exact binary64 test in the contract's
+// operation order.  Decisions are therefore the binary64 contract's.
 // d is returned; alpha is consumed only after z (hides its load latency).
 __device__ __forceinline__ bool mt_trial(uint4 w, double alpha, double& d, double& g) {
-  const double L = log(1.0 - u53(w.x, w.y));
-  const double z = __dmul_rn(sqrt(-2.0 * L), cospi(2.0 * u32d(w.z)));
+  const double L = dm::ln_pos(dm::one_minus_u53(w.x, w.y));
+  const double z = __dmul_rn(dm::sqrt_nonneg(-2.0 * L), dm::cos2pi_u32(w.z));
   double c;
   mt_consts(alpha, d, c);
   const double cz = __dmul_rn(c, z);
@@ -105,24 +251,13 @@ __device__ __forceinline__ bool mt_trial(uint4 w, double alpha, double& d, doubl
   if (!(t > 0.0)) return false;
   const double v = __dmul_rn(__dmul_rn(t, t), t);
   g = __dmul_rn(d, v);
-  const double U = 1.0 - u32d(w.w);
-  const double wv = cz * (3.0 + cz * (3.0 + cz));
-  const float wf = (float)wv;
-  const float lf = log1pf(wf) - wf;
-  const float lnu = logf((float)U);
-  const double z2h = 0.5 * z * z;
-  const double m = fma(d, (double)lf, z2h) - (double)lnu;
-  const double band = 1e-5 * (1.0 + z2h + d * fabs(wv) + fabs((double)lnu));
-  if (m > band) return true;
-  if (m < -band) return false;
-  const double rhs = __dadd_rn(__dsub_rn(__dadd_rn(__dmul_rn(__dmul_rn(z, z), 0.5), d),
-                                         __dmul_rn(d, v)),
-                               __dmul_rn(d, log(v)));
-  return log(U) < rhs;
+  const int sc = mt_screen(z, d, t, w.w);
+  if (sc != 0) return sc > 0;
+  return mt_exact(z, d, v, w.w);
 }
 // alpha < 1 boost (R-10): g * exp(ln(1-u53(w0,w1)) / alpha) from block 256 i.
 __device__ __forceinline__ double mt_boost(uint4 wb, double g, double alpha) {
-  return g * exp(log(1.0 - u53(wb.x, wb.y)) / alpha);
+  return g * dm::exp_nonpos(dm::ln_pos(dm::one_minus_u53(wb.x, wb.y)) / alpha);
 }
 
 // ---- per-sample getters: value of sample i of the bulk call at cursor base --------

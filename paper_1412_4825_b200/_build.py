@@ -27,6 +27,7 @@ def _stale() -> bool:
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "brng.h"))
     deps.append(os.path.join(ROOT, "include", "brng_device.cuh"))
+    deps.append(os.path.join(ROOT, "include", "brng_device_tables.cuh"))
     deps.append(__file__)
     return any(os.path.getmtime(d) > t for d in deps)
 

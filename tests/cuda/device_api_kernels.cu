@@ -55,6 +55,39 @@ __global__ void k_gibbs(uint64_t seed, uint64_t stream_id, uint64_t base, uint64
     out_y[s * n_chains + c] = y;
   }
 }
+// The table-driven binary64 math of the Gamma path (brng_dev::dm), one
+// function per `fn`: 0 ln_pos(x), 1 cos2pi_u32(w), 2 exp_nonpos(x),
+// 3 one_minus_u53(w[2i], w[2i+1]), 4 rsqrt_pos(x), 5 sqrt_nonneg(x).
+__global__ void k_math(int fn, const double* x, const uint32_t* w, double* out, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  namespace dm = brng_dev::dm;
+  out[i] = fn == 0 ? dm::ln_pos(x[i])
+         : fn == 1 ? dm::cos2pi_u32(w[i])
+         : fn == 2 ? dm::exp_nonpos(x[i])
+         : fn == 3 ? dm::one_minus_u53(w[2 * i], w[2 * i + 1])
+         : fn == 4 ? dm::rsqrt_pos(x[i])
+                   : dm::sqrt_nonneg(x[i]);
+}
+// The Marsaglia-Tsang decision pieces on given Philox words: the binary32
+// screen (+1/-1/0) and the exact binary64 test, for trials with 1 + cz > 0
+// (screen = 2 marks 1 + cz <= 0).  Same steps as brng_dev::mt_trial.
+__global__ void k_screen(const uint32_t* w, const double* alpha, signed char* screen,
+                         signed char* exact, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  namespace dm = brng_dev::dm;
+  const uint4 b = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+  const double L = dm::ln_pos(dm::one_minus_u53(b.x, b.y));
+  const double z = __dmul_rn(dm::sqrt_nonneg(-2.0 * L), dm::cos2pi_u32(b.z));
+  double d, c;
+  brng_dev::mt_consts(alpha[i], d, c);
+  const double t = __dadd_rn(1.0, __dmul_rn(c, z));
+  if (!(t > 0.0)) { screen[i] = 2; exact[i] = 0; return; }
+  const double v = __dmul_rn(__dmul_rn(t, t), t);
+  screen[i] = (signed char)brng_dev::mt_screen(z, d, t, b.w);
+  exact[i] = brng_dev::mt_exact(z, d, v, b.w) ? 1 : 0;
+}
 unsigned grid(uint64_t n) { return (unsigned)((n + 255) / 256); }
 }  // namespace
 
@@ -72,6 +105,15 @@ int dev_fill32(int dist, uint64_t seed, uint64_t stream, uint64_t base, const fl
 int dev_gamma(uint64_t seed, uint64_t stream, uint64_t base, const double* a, const double* b,
               double* out, unsigned char* tr, uint64_t n, void* s) {
   k_gamma<<<grid(n), 256, 0, (cudaStream_t)s>>>(seed, stream, base, a, b, out, tr, n);
+  return (int)cudaGetLastError();
+}
+int dev_math(int fn, const double* x, const uint32_t* w, double* out, uint64_t n, void* s) {
+  k_math<<<grid(n), 256, 0, (cudaStream_t)s>>>(fn, x, w, out, n);
+  return (int)cudaGetLastError();
+}
+int dev_screen(const uint32_t* w, const double* alpha, signed char* screen, signed char* exact,
+               uint64_t n, void* s) {
+  k_screen<<<grid(n), 256, 0, (cudaStream_t)s>>>(w, alpha, screen, exact, n);
   return (int)cudaGetLastError();
 }
 int dev_gibbs(uint64_t seed, uint64_t stream_id, uint64_t base, uint64_t nc, uint64_t ns,

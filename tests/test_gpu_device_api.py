@@ -112,3 +112,170 @@ def test_fig1_user_gibbs_loop_matches_oracle_and_bulk(user_lib):
     r = oracle.gibbs_triangle(42, 0, 0, nc, ns)
     assert np.array_equal(ox.cpu().numpy(), r["out_x"])
     assert np.array_equal(oy.cpu().numpy(), r["out_y"])
+
+
+# ---- table-driven binary64 math of the Gamma path (brng_dev::dm) -----------------
+def _math(user_lib, fn, x=None, w=None, n=None):
+    n = n if n is not None else len(x) if x is not None else len(w)
+    xd = torch.tensor(x if x is not None else [0.0], dtype=torch.float64, device=dev())
+    wd = torch.tensor(np.asarray(w if w is not None else [0], dtype=np.uint32).view(np.int32),
+                      device=dev())
+    out = torch.empty(n, dtype=torch.float64, device=dev())
+    L = user_lib
+    L.dev_math.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                           C.c_void_p]
+    assert L.dev_math(fn, xd.data_ptr(), wd.data_ptr(), out.data_ptr(), n, _s()) == 0
+    return out.cpu().numpy()
+
+
+def _ulp_err(got, exact):
+    import math
+    return [abs(float(g) - float(e)) / math.ulp(float(e)) if e != 0 else abs(float(g))
+            for g, e in zip(got, exact)]
+
+
+def test_dm_ln_pos_accuracy(user_lib):
+    """ln(1 - u53) over the trial's whole argument range [2^-53, 1] (and any
+    positive normal) within 2.5 ulp of the mpmath value; exactly 0 at 1 and
+    relative-accurate next to 1."""
+    import mpmath as mp
+    mp.mp.dps = 40
+    rng = np.random.default_rng(1)
+    k = np.concatenate([[0, 1, 2, 3, 2**52, 2**52 - 1, 2**53 - 1, 2**53 - 2],
+                        rng.integers(0, 2**53, 3000, dtype=np.int64),
+                        rng.integers(0, 2**20, 500, dtype=np.int64),
+                        (2**53 - rng.integers(1, 2**20, 500, dtype=np.int64))])
+    x = [(2**53 - int(v)) * 2.0**-53 for v in k]
+    x += list(np.exp(rng.uniform(-690, 690, 1000)))
+    x += [float(np.sqrt(0.5)), float(np.nextafter(np.sqrt(0.5), 0)), float(np.sqrt(2.0)),
+          1.0 + 1.0 / 256, 1.0 - 1.0 / 256, 2.0**-1022]
+    got = _math(user_lib, 0, x=x)
+    exact = [mp.log(mp.mpf(v)) for v in x]
+    err = _ulp_err(got, exact)
+    assert got[0] == 0.0
+    assert max(err) <= 2.5, (max(err), x[int(np.argmax(err))])
+
+
+def test_dm_cos2pi_u32_accuracy(user_lib):
+    """cos(2 pi w / 2^32) for 32-bit w (the trial's angle): absolute error
+    <= 2^-53 everywhere, exact values at the quarter turns and relative
+    accuracy next to the zeros of cos."""
+    import mpmath as mp
+    mp.mp.dps = 40
+    rng = np.random.default_rng(2)
+    special = [0, 1 << 30, 1 << 31, 3 << 30, (1 << 30) + 1, (1 << 30) - 1, (3 << 30) + 7,
+               (1 << 23) - 1, 1 << 23, (1 << 23) + 1, 0xFFFFFFFF, 0xFF800000, 0x7FFFFFFF]
+    w = special + list(rng.integers(0, 2**32, 5000, dtype=np.uint64))
+    got = _math(user_lib, 1, w=w)
+    exact = [mp.cos(2 * mp.pi * int(v) / mp.mpf(2) ** 32) for v in w]
+    abs_err = [abs(float(g) - float(e)) for g, e in zip(got, exact)]
+    assert max(abs_err) <= 2.0**-53, max(abs_err)
+    assert list(got[:4]) == [1.0, 0.0, -1.0, 0.0]
+    for idx in (4, 5, 6):       # next to a zero: relative accuracy
+        assert abs(float(got[idx]) - float(exact[idx])) <= 2 * abs(float(exact[idx])) * 2.0**-52
+
+
+def test_dm_exp_nonpos_accuracy(user_lib):
+    """e^y for y <= 0 (the boost's ln(1-u)/alpha) within 2 ulp in the normal
+    range, exact at 0, and through libdevice below -700 (subnormal results)."""
+    import mpmath as mp
+    mp.mp.dps = 40
+    rng = np.random.default_rng(3)
+    y = [0.0, -0.0, -1e-300, -2.0**-60, -1e-10, -0.5, -1.0, -700.0, -700.0 - 2**-40, -708.5,
+         -745.0, -800.0, float(np.log(0.5))]
+    y += list(-rng.exponential(20.0, 3000)) + list(-rng.uniform(0, 0.01, 500))
+    got = _math(user_lib, 2, x=y)
+    exact = [mp.exp(mp.mpf(v)) for v in y]
+    assert got[0] == 1.0 and got[1] == 1.0
+    import math
+    for g, e, v in zip(got, exact, y):
+        e = float(e)
+        if e >= 2.0**-1022:
+            assert abs(float(g) - e) <= 2 * math.ulp(e), (v, g, e)
+        else:
+            assert abs(float(g) - e) <= math.ulp(0.0) * 2, (v, g, e)
+
+
+def test_dm_one_minus_u53_exact(user_lib):
+    """1 - u53 built from the word bits equals fl(1 - u53(lo, hi)) exactly
+    (no rounding happens in either), including k = 0, 1, 2^52, 2^53 - 1."""
+    rng = np.random.default_rng(4)
+    pairs = [(0, 0), (0x800, 0), (0, 0x80000000), (0xFFFFFFFF, 0xFFFFFFFF), (0x7FF, 0),
+             (0xFFFFF800, 0x7FFFFFFF), (0, 0x00100000)]
+    pairs += [tuple(int(v) for v in rng.integers(0, 2**32, 2, dtype=np.uint64))
+              for _ in range(5000)]
+    w = [v for p in pairs for v in p]
+    got = _math(user_lib, 3, w=w, n=len(pairs))
+    for (lo, hi), g in zip(pairs, got):
+        k = ((hi << 32) | lo) >> 11
+        assert float(g) == (2**53 - k) / 2**53, (lo, hi)
+
+
+def test_dm_rsqrt_sqrt_accuracy(user_lib):
+    """rsqrt_pos within 1.5 ulp and sqrt_nonneg within 2.5 ulp of mpmath on
+    the trial's arguments (9d in [6, 1800], -2 ln(1-u) in [0, 74]) and
+    across exponents; sqrt_nonneg(0) = 0."""
+    import mpmath as mp
+    mp.mp.dps = 40
+    rng = np.random.default_rng(5)
+    x = [6.0, 1800.0, 2.0**-53 * 2, 73.7, 1.0, 4.0, float(np.nextafter(1.0, 2.0))]
+    x += list(rng.uniform(6, 1800, 2000)) + list(np.exp(rng.uniform(-700, 700, 2000)))
+    r = _math(user_lib, 4, x=x)
+    err = _ulp_err(r, [1 / mp.sqrt(mp.mpf(v)) for v in x])
+    assert max(err) <= 1.5, (max(err), x[int(np.argmax(err))])
+    xs = [0.0] + list(-2 * np.log1p(-rng.uniform(0, 1, 3000))) + x
+    s = _math(user_lib, 5, x=xs)
+    assert s[0] == 0.0
+    err = _ulp_err(s[1:], [mp.sqrt(mp.mpf(v)) for v in xs[1:]])
+    assert max(err) <= 2.5, (max(err), xs[1 + int(np.argmax(err))])
+
+
+def _screen(user_lib, words, alpha):
+    n = len(alpha)
+    wd = torch.tensor(words.astype(np.uint32).view(np.int32), device=dev())
+    ad = torch.tensor(alpha, dtype=torch.float64, device=dev())
+    sc = torch.empty(n, dtype=torch.int8, device=dev())
+    ex = torch.empty(n, dtype=torch.int8, device=dev())
+    user_lib.dev_screen.argtypes = [C.c_void_p] * 4 + [C.c_uint64, C.c_void_p]
+    assert user_lib.dev_screen(wd.data_ptr(), ad.data_ptr(), sc.data_ptr(), ex.data_ptr(), n,
+                               _s()) == 0
+    return sc.cpu().numpy(), ex.cpu().numpy()
+
+
+@pytest.mark.parametrize("alpha_lo,alpha_hi,undecided", [(1.0, 1.5, 0.002), (1.0, 200.0, 0.01),
+                                                         (150.0, 1e4, 0.05)])
+def test_mt_screen_sound_at_the_boundary(user_lib, alpha_lo, alpha_hi, undecided):
+    """The binary32 screen of the M-T acceptance test never contradicts the
+    exact binary64 test.  Adversarial inputs: U is placed within a few 2^-32
+    steps of exp(rhs), i.e. on the acceptance boundary, so every screen
+    error would show; random inputs: the screen leaves few trials undecided
+    (the band grows with d: < 1% up to the configs' alpha = 200)."""
+    rng = np.random.default_rng(6)
+    n = 400_000
+    words = rng.integers(0, 2**32, (n, 4), dtype=np.uint64)
+    alpha = np.exp(rng.uniform(np.log(alpha_lo), np.log(alpha_hi), n))
+    # random words: decided almost always, never wrong
+    sc, ex = _screen(user_lib, words.ravel(), alpha)
+    live = sc != 2
+    assert np.all((sc[live] == 0) | ((sc[live] > 0) == (ex[live] == 1)))
+    assert np.mean(sc[live] == 0) < undecided
+    # boundary words: w3 such that U = 1 - w3 2^-32 ~ exp(rhs) (host fp64 estimate)
+    k = ((words[:, 1] << np.uint64(32)) | words[:, 0]) >> np.uint64(11)
+    L = np.log((2.0**53 - k.astype(np.float64)) / 2.0**53)
+    z = np.sqrt(-2 * L) * np.cos(2 * np.pi * words[:, 2].astype(np.float64) / 2.0**32)
+    d = alpha - 1.0 / 3.0
+    t = 1 + z / np.sqrt(9 * d)
+    ok = t > 1e-3
+    v = t**3
+    rhs = 0.5 * z * z + d - d * v + d * np.log(np.where(ok, v, 1.0))
+    ok &= (rhs < -1e-6) & (rhs > -20)
+    w3 = np.round((1 - np.exp(rhs)) * 2.0**32) + rng.integers(-3, 4, n)
+    ok &= (w3 >= 0) & (w3 < 2**32)
+    words[:, 3] = np.where(ok, w3, 0).astype(np.uint64)
+    sel = np.nonzero(ok)[0]
+    sc, ex = _screen(user_lib, words[sel].ravel(), alpha[sel])
+    live = sc != 2
+    assert live.sum() > 0.5 * len(sel)
+    bad = (sc[live] != 0) & ((sc[live] > 0) != (ex[live] == 1))
+    assert not bad.any(), int(bad.sum())
+    assert np.mean(sc[live] == 0) > 0.5      # the boundary really was hit
