@@ -99,6 +99,7 @@ enum {
   kLn2Hi, kLn2Lo, kRndM128, kI2dBias,    // ln 2 split; 1.5*2^52 - 128; 2^52 + 2^31
   kS7, kS5, kS3, kC6, kC4, kTwoPi32,     // sin/cos Taylor; 2 pi / 2^32
   kE6, kE5, kE4, kE3, kInvLn2x64, kLn2Hi64, kLn2Lo64, kRnd,
+  kNewton3, kThird,                      // 3/8 (rsqrt step); 1/3 (M-T d)
   kNumConst
 };
 static __constant__ double kC[kNumConst] = {
@@ -112,6 +113,7 @@ static __constant__ double kC[kNumConst] = {
     0x1.71547652b82fep+6,            // 64 / ln 2
     0x1.62e42feep-7, 0x1.a39ef35793c76p-39,   // ln2_hi / 64, ln2_lo / 64
     6755399441055744.0,              // 1.5 * 2^52: round-to-integer shifter
+    0.375, 1.0 / 3.0,
 };
 // exact binary64 of a 32-bit signed integer without the I2F pipe
 __device__ __forceinline__ double i2d(int v) {
@@ -184,7 +186,7 @@ __device__ __forceinline__ double rsqrt_pos(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double e = fma(-x * y, y, 1.0);
-  return fma(y * e, fma(e, 0.375, 0.5), y);
+  return fma(y * e, fma(e, kC[kNewton3], 0.5), y);
 }
 // sqrt(x) for x = 0 or a positive normal: x * rsqrt(x) (~2 ulp).
 __device__ __forceinline__ double sqrt_nonneg(double x) {
@@ -197,13 +199,31 @@ __device__ __forceinline__ float ln_approx_f32(float x) {
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(x));
   return l * 0.69314718f;
 }
+// {sin, cos}(2 pi u24(w)), u24(w) = (w >> 8) 2^-24, in binary32: k = w >> 8,
+// j = round(k / 2^18) mod 64, b = 2 pi (k - j 2^18) 2^-24 (|b| <= pi/64);
+// table {C_j, S_j} (exact 0/+-1 at the quarter turns, so results near the
+// zeros of sin/cos are relative-accurate) and Taylor sin b to b^5, cos b - 1
+// to b^4 (truncation < 2e-11).  ~1e-7 absolute, vs ~3x the instructions of
+// sincospif.
+__device__ __forceinline__ void sincos2pi_u24(uint32_t w, float* sn, float* cs) {
+  const uint32_t k = w >> 8;
+  const uint32_t j = ((k + 0x20000u) >> 18) & 63u;
+  const int rem = (int)((k - (j << 18)) << 14) >> 14;   // sign-extended 18 bits
+  const float b = (float)rem * 0x1.921fb6p-22f;          // 2 pi / 2^24
+  const float2 t = __ldg(&tab::kSinCos32[j]);
+  const float b2 = b * b;
+  const float sb = fmaf(b2 * b, fmaf(b2, 1.0f / 120.0f, -1.0f / 6.0f), b);
+  const float cm1 = b2 * fmaf(b2, 1.0f / 24.0f, -0.5f);
+  *cs = t.x + fmaf(t.x, cm1, -t.y * sb);
+  *sn = t.y + fmaf(t.y, cm1, t.x * sb);
+}
 }  // namespace dm
 
 // ---- Marsaglia-Tsang trial (R-08, R-09) -----------------------------------------
 // d = alpha' - 1/3, c = 1/sqrt(9 d) (~1 ulp).
 __device__ __forceinline__ void mt_consts(double alpha, double& d, double& c) {
   const double ap = alpha < 1.0 ? alpha + 1.0 : alpha;
-  d = ap - 1.0 / 3.0;
+  d = ap - dm::kC[dm::kThird];
   c = dm::rsqrt_pos(9.0 * d);
 }
 // The binary32 screen of the acceptance test (see mt_trial): +1 accept,
@@ -291,7 +311,7 @@ __device__ __forceinline__ float std_gaussian_f32(const Key& k, uint64_t stream,
   const int p = (int)((i % 4) / 2);
   const float r = sqrtf(-2.0f * logf(1.0f - u24(word(w, 2 * p))));
   float sn, cs;
-  sincospif(2.0f * u24(word(w, 2 * p + 1)), &sn, &cs);
+  dm::sincos2pi_u24(word(w, 2 * p + 1), &sn, &cs);
   return (i % 2) ? r * sn : r * cs;
 }
 __device__ __forceinline__ double std_gaussian_f64(const Key& k, uint64_t stream, uint64_t base,

@@ -29,7 +29,7 @@ struct FillArgs {
   uint64_t n;
   uint64_t base;
   uint64_t stream;
-  uint32_t k0, k1;
+  RoundKeys rk;  // Philox round keys (constant bank)
   int vec;       // all arrays aligned to the vector width
   unsigned long long* err;
   T s0, s1;      // SCALAR mode: fixed parameters (the paper's VSL-Batch case)
@@ -123,10 +123,10 @@ __device__ __forceinline__ void std_block(uint4 w, float* s) {
   if (DIST == kGaussian) {
     float sn, cs;
     const float r0 = sqrtf(-2.0f * logf(1.0f - u24(w.x)));
-    sincospif(2.0f * u24(w.y), &sn, &cs);
+    brng_dev::dm::sincos2pi_u24(w.y, &sn, &cs);
     s[0] = r0 * cs; s[1] = r0 * sn;
     const float r1 = sqrtf(-2.0f * logf(1.0f - u24(w.z)));
-    sincospif(2.0f * u24(w.w), &sn, &cs);
+    brng_dev::dm::sincos2pi_u24(w.w, &sn, &cs);
     s[2] = r1 * cs; s[3] = r1 * sn;
   } else if (DIST == kLaplace) {
     const float e0 = -logf(1.0f - u24(w.x)), e1 = -logf(1.0f - u24(w.z));
@@ -176,7 +176,7 @@ constexpr int kBPT = BRNG_FILL_BPT;    // Philox blocks per thread per iteration
 // Each thread handles kBPT blocks per iteration (stride apart): all parameter
 // loads are issued before any Philox work, for memory-level parallelism.
 template <typename T, int DIST, bool SCALAR = false>
-__global__ void __launch_bounds__(kThreads) fill_kernel(FillArgs<T> a) {
+__global__ void __launch_bounds__(kThreads) fill_kernel(const __grid_constant__ FillArgs<T> a) {
   constexpr int S = spb<T, DIST>();
   constexpr int NP = SCALAR ? 0 : n_params<DIST>();
   const uint64_t nblk = (a.n + S - 1) / S;
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kThreads) fill_kernel(FillArgs<T> a) {
     for (int b = 0; b < kBPT; ++b) {
       const uint64_t j = j0 + b * stride;
       if (j >= nblk) break;
-      const uint4 w = philox_block(a.base + j, a.stream, a.k0, a.k1);
+      const uint4 w = philox_block_rk(a.base + j, a.stream, a.rk);
       T s[S];
       std_block<DIST>(w, s);
       const uint64_t i0 = j * S;
@@ -227,11 +227,11 @@ __global__ void __launch_bounds__(kThreads) fill_kernel(FillArgs<T> a) {
   if (SCALAR || NP > 0) flush_errors(a.err, bad);
 }
 
-__global__ void __launch_bounds__(kThreads) raw_u32_kernel(FillArgs<uint32_t> a) {
+__global__ void __launch_bounds__(kThreads) raw_u32_kernel(const __grid_constant__ FillArgs<uint32_t> a) {
   const uint64_t nblk = (a.n + 3) >> 2;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   for (uint64_t j = (uint64_t)blockIdx.x * kThreads + threadIdx.x; j < nblk; j += stride) {
-    const uint4 w = philox_block(a.base + j, a.stream, a.k0, a.k1);
+    const uint4 w = philox_block_rk(a.base + j, a.stream, a.rk);
     const uint64_t i0 = j << 2;
     if (a.vec && i0 + 4 <= a.n) {
       __stcs(reinterpret_cast<uint4*>(a.out) + j, w);
@@ -258,7 +258,7 @@ cudaError_t run_dist(const T* p0, const T* p1, T* out, uint64_t n, uint64_t base
                      const Ctx& ctx, const double* scalars) {
   constexpr int S = spb<T, DIST>();
   const uintptr_t vb = sizeof(T) * S;
-  FillArgs<T> a{p0, p1, out, n, base, ctx.stream_id, ctx.k0, ctx.k1,
+  FillArgs<T> a{p0, p1, out, n, base, ctx.stream_id, make_round_keys(ctx.k0, ctx.k1),
                 aligned(p0, vb) && aligned(p1, vb) && aligned(out, vb), ctx.err, T(0), T(0)};
   const unsigned g = grid_for((n + S - 1) / S, ctx);
   if (scalars) {
@@ -298,7 +298,7 @@ cudaError_t launch_fill(int dist, int dtype, const void* p0, const void* p1, voi
                         uint64_t n, uint64_t base, const Ctx& ctx, const double* scalars) {
   if (dist == kRaw) {
     FillArgs<uint32_t> a{nullptr, nullptr, static_cast<uint32_t*>(out), n, base, ctx.stream_id,
-                         ctx.k0, ctx.k1, aligned(out, 16), ctx.err};
+                         make_round_keys(ctx.k0, ctx.k1), aligned(out, 16), ctx.err};
     raw_u32_kernel<<<grid_for((n + 3) >> 2, ctx), kThreads, 0, ctx.stream>>>(a);
     return cudaGetLastError();
   }

@@ -53,7 +53,7 @@ constexpr int kBoostCap = 64;
 // iteration, queued or not) never changes it.
 template <typename Load, typename Sink>
 __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t base,
-                                         uint64_t stream, uint32_t k0, uint32_t k1, Load load,
+                                         uint64_t stream, const RoundKeys& rk, Load load,
                                          Sink sink, uint32_t& nbad, BoostItem* q) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
@@ -75,7 +75,7 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
     if (lane < n) {
       const BoostItem it = q[qn - n + lane];
       const uint64_t ii = it.i_t & 0x00FFFFFFFFFFFFFFull;
-      const uint4 wb = philox_block(base + (uint64_t)kStride * ii, stream, k0, k1);
+      const uint4 wb = philox_block_rk(base + (uint64_t)kStride * ii, stream, rk);
       const double gb = mt_boost(wb, it.g, it.alpha);
       sink(ii, gb * it.beta, (uint32_t)(it.i_t >> 56));
     }
@@ -87,7 +87,7 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
     bool done = false, boost = false;
     double g = 0.0;
     if (active) {
-      const uint4 w = philox_block(base + (uint64_t)kStride * i + t, stream, k0, k1);
+      const uint4 w = philox_block_rk(base + (uint64_t)kStride * i + t, stream, rk);
       const bool valid = isfinite(alpha) && isfinite(beta) && alpha > 0.0 && beta > 0.0;
       const bool acc = mt_trial(w, alpha, d, g);
       if (!valid) {
@@ -127,7 +127,7 @@ struct GammaArgs {
   T* out;
   uint8_t* trials;
   uint64_t n, base, stream;
-  uint32_t k0, k1;
+  RoundKeys rk;
   unsigned long long* err;
 };
 
@@ -135,7 +135,7 @@ template <typename T>
 #ifndef BRNG_GAMMA_MINB
 #define BRNG_GAMMA_MINB 4
 #endif
-__global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(GammaArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(const __grid_constant__ GammaArgs<T> a) {
   __shared__ BoostItem qs[kThreads / 32][kBoostCap];
   BoostItem* q = qs[threadIdx.x >> 5];
   const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(GammaA
   for (uint64_t beg = warp * kChunk; beg < a.n; beg += n_warps * kChunk) {
     const uint64_t end = beg + kChunk < a.n ? beg + kChunk : a.n;
     mt_queue(
-        beg, end, a.base, a.stream, a.k0, a.k1,
+        beg, end, a.base, a.stream, a.rk,
         [&](uint64_t i, double& al, double& be) {
           al = (double)__ldg(a.alpha + i);
           be = (double)__ldg(a.beta + i);
@@ -164,7 +164,7 @@ struct DirArgs {
   T* out;
   uint8_t* trials;
   uint64_t n_rows, k, base, stream;
-  uint32_t k0, k1;
+  RoundKeys rk;
   unsigned long long* err;
 };
 
@@ -181,7 +181,7 @@ __device__ __forceinline__ double warp_sum(double s) {
 // summed lane-strided then by a fixed xor-shuffle tree, normalised, stored
 // coalesced.
 template <typename T>
-__global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(DirArgs<T> a) {
+__global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __grid_constant__ DirArgs<T> a) {
   extern __shared__ double gsm[];
   __shared__ BoostItem qs[kDirThreads / 32][kBoostCap];
   BoostItem* q = qs[threadIdx.x >> 5];
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(DirArgs<T> 
   for (uint64_t row = warp; row < a.n_rows; row += n_warps) {
     const uint64_t beg = row * a.k;
     mt_queue(
-        beg, beg + a.k, a.base, a.stream, a.k0, a.k1,
+        beg, beg + a.k, a.base, a.stream, a.rk,
         [&](uint64_t i, double& al, double& be) {
           al = (double)__ldg(a.alpha + i);
           be = 1.0;
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(DirArgs<T> 
 // Any K: two passes over the row's Gamma samples (the second recomputes them
 // from their counters -- exact, no scratch).
 template <typename T>
-__global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(DirArgs<T> a) {
+__global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(const __grid_constant__ DirArgs<T> a) {
   __shared__ BoostItem qs[kDirThreads / 32][kBoostCap];
   BoostItem* q = qs[threadIdx.x >> 5];
   const uint64_t warp = ((uint64_t)blockIdx.x * kDirThreads + threadIdx.x) >> 5;
@@ -230,11 +230,11 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(DirArgs<T>
       be = 1.0;
     };
     double s = 0.0;
-    mt_queue(beg, beg + a.k, a.base, a.stream, a.k0, a.k1, load,
+    mt_queue(beg, beg + a.k, a.base, a.stream, a.rk, load,
              [&](uint64_t, double v, uint32_t) { s += v; }, nbad, q);
     s = warp_sum(s);
     const double inv = 1.0 / s;
-    mt_queue(beg, beg + a.k, a.base, a.stream, a.k0, a.k1, load,
+    mt_queue(beg, beg + a.k, a.base, a.stream, a.rk, load,
              [&](uint64_t i, double v, uint32_t t) {
                a.out[i] = (T)(v * inv);
                if (a.trials) a.trials[i] = (uint8_t)t;
@@ -247,7 +247,8 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(DirArgs<T>
 template <typename T>
 cudaError_t gamma_typed(const T* alpha, const T* beta, T* out, uint8_t* trials, uint64_t n,
                         uint64_t base, const Ctx& ctx) {
-  GammaArgs<T> a{alpha, beta, out, trials, n, base, ctx.stream_id, ctx.k0, ctx.k1, ctx.err};
+  GammaArgs<T> a{alpha, beta, out, trials, n, base, ctx.stream_id,
+                   make_round_keys(ctx.k0, ctx.k1), ctx.err};
   const uint64_t warps_needed = (n + kChunk - 1) / kChunk;
   const uint64_t ctas_needed = (warps_needed + (kThreads / 32) - 1) / (kThreads / 32);
   const uint64_t cap = (uint64_t)ctx.num_sms * 8;  // one full-occupancy wave
@@ -259,7 +260,8 @@ cudaError_t gamma_typed(const T* alpha, const T* beta, T* out, uint8_t* trials, 
 template <typename T>
 cudaError_t dirichlet_typed(const T* alpha, uint64_t n_rows, uint64_t k, T* out,
                             uint8_t* trials, uint64_t base, const Ctx& ctx) {
-  DirArgs<T> a{alpha, out, trials, n_rows, k, base, ctx.stream_id, ctx.k0, ctx.k1, ctx.err};
+  DirArgs<T> a{alpha, out, trials, n_rows, k, base, ctx.stream_id,
+                 make_round_keys(ctx.k0, ctx.k1), ctx.err};
   const uint64_t ctas_needed = (n_rows + 3) / 4;
   if (k <= kDirSmemK) {
     const size_t smem = (size_t)4 * k * sizeof(double);

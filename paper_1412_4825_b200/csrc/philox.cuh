@@ -27,6 +27,30 @@ using brng_dev::u24;
 using brng_dev::u32d;
 using brng_dev::u53;
 
+// Round keys k + r W (mod 2^32) of the 10 rounds, computed on the host and
+// passed in a __grid_constant__ kernel argument: the LOP3s of every round then
+// read them straight from the constant bank (no per-block key schedule, no
+// registers).  Bit-identical to philox_block(pos, stream, k0, k1).
+struct RoundKeys {
+  uint32_t k0[10], k1[10];
+};
+inline RoundKeys make_round_keys(uint32_t k0, uint32_t k1) {
+  RoundKeys rk;
+  for (int r = 0; r < 10; ++r) {
+    rk.k0[r] = k0 + (uint32_t)r * kPhiloxW0;
+    rk.k1[r] = k1 + (uint32_t)r * kPhiloxW1;
+  }
+  return rk;
+}
+__device__ __forceinline__ uint4 philox_block_rk(uint64_t pos, uint64_t stream,
+                                                 const RoundKeys& rk) {
+  uint4 c = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)stream,
+                       (uint32_t)(stream >> 32));
+#pragma unroll
+  for (int r = 0; r < 10; ++r) c = philox_round(c, rk.k0[r], rk.k1[r]);
+  return c;
+}
+
 // ---- warp helpers -----------------------------------------------------------
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;

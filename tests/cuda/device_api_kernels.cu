@@ -57,7 +57,8 @@ __global__ void k_gibbs(uint64_t seed, uint64_t stream_id, uint64_t base, uint64
 }
 // The table-driven binary64 math of the Gamma path (brng_dev::dm), one
 // function per `fn`: 0 ln_pos(x), 1 cos2pi_u32(w), 2 exp_nonpos(x),
-// 3 one_minus_u53(w[2i], w[2i+1]), 4 rsqrt_pos(x), 5 sqrt_nonneg(x).
+// 3 one_minus_u53(w[2i], w[2i+1]), 4 rsqrt_pos(x), 5 sqrt_nonneg(x),
+// 6/7 sin/cos of sincos2pi_u24(w) (binary32).
 __global__ void k_math(int fn, const double* x, const uint32_t* w, double* out, uint64_t n) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -67,7 +68,13 @@ __global__ void k_math(int fn, const double* x, const uint32_t* w, double* out, 
          : fn == 2 ? dm::exp_nonpos(x[i])
          : fn == 3 ? dm::one_minus_u53(w[2 * i], w[2 * i + 1])
          : fn == 4 ? dm::rsqrt_pos(x[i])
-                   : dm::sqrt_nonneg(x[i]);
+         : fn == 5 ? dm::sqrt_nonneg(x[i])
+                   : 0.0;
+  if (fn == 6 || fn == 7) {
+    float sn, cs;
+    dm::sincos2pi_u24(w[i], &sn, &cs);
+    out[i] = fn == 6 ? (double)sn : (double)cs;
+  }
 }
 // The Marsaglia-Tsang decision pieces on given Philox words: the binary32
 // screen (+1/-1/0) and the exact binary64 test, for trials with 1 + cz > 0

@@ -279,3 +279,27 @@ def test_mt_screen_sound_at_the_boundary(user_lib, alpha_lo, alpha_hi, undecided
     bad = (sc[live] != 0) & ((sc[live] > 0) != (ex[live] == 1))
     assert not bad.any(), int(bad.sum())
     assert np.mean(sc[live] == 0) > 0.5      # the boundary really was hit
+
+
+def test_dm_sincos2pi_u24_accuracy(user_lib):
+    """binary32 {sin, cos}(2 pi (w>>8) 2^-24) (the f32 Box-Muller angle):
+    absolute error <= 1.2e-7, exact at the quarter turns, and relative error
+    <= 4 ulp wherever |value| >= 2^-8 or the angle is next to a quarter turn."""
+    import mpmath as mp
+    mp.mp.dps = 30
+    rng = np.random.default_rng(7)
+    q = [0, 1 << 30, 1 << 31, 3 << 30]
+    near = [v + (d << 8) for v in q for d in (1, 2, 3, -1, -2, 5000, -5000)]
+    w = q + [v % 2**32 for v in near] + list(rng.integers(0, 2**32, 6000, dtype=np.uint64))
+    w = [int(v) for v in w]
+    sn, cs = _math(user_lib, 6, w=w), _math(user_lib, 7, w=w)
+    ang = [2 * mp.pi * (v >> 8) / mp.mpf(2) ** 24 for v in w]
+    es, ec = [float(mp.sin(a)) for a in ang], [float(mp.cos(a)) for a in ang]
+    assert list(sn[:4]) == [0.0, 1.0, 0.0, -1.0] and list(cs[:4]) == [1.0, 0.0, -1.0, 0.0]
+    for got, ex in ((sn, es), (cs, ec)):
+        err = np.abs(got - np.array(ex))
+        assert err.max() <= 1.2e-7, err.max()
+        big = np.abs(ex) >= 2.0**-8
+        big[4:4 + len(near)] = True
+        rel = err[big] / np.abs(np.array(ex)[big])
+        assert rel.max() <= 4 * 2.0**-24, rel.max()
