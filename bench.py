@@ -46,12 +46,18 @@ SMS, SMSP, LANES = 148, 4, 32
 # 5 statistics) = 17*2 + 9 = 43 fp64-pipe slots; peak = 64 x 148 x f_sm.
 GIBBS_PIPE_OPS_PER_SWEEP = 43
 FP64_LANES_PER_SM = 64
-# Per Gamma sample: E[trials] x (Philox 40 + u53 5 + log 30 + sqrt
-# 12 + cospi 25 + test 10) + P(alpha<1) x (Philox 40 + u53 5 + log 30 + div 15
-# + exp 20) + load/store/queue 12 -- evaluated from the measured trial mix.
-GAMMA_TRIAL_INSTR = 122
-GAMMA_BOOST_INSTR = 110
-GAMMA_SAMPLE_INSTR = 12
+# Gamma / Dirichlet roofline (DESIGN.md §7 K3): the same FMA-heavy pipe as
+# Gibbs.  Algorithmic slots of the method as implemented (fp64 ops + 2 per
+# IMAD.WIDE), counted from the kernel's arithmetic:
+#   trial = Philox 19 IMAD.WIDE (38) + 1-u53 1 + ln 14 + sqrt 7 + cos 13
+#           + d, c 8 + cz, t, v, g 5 + z, -2L 2                      = 88
+#   boost = Philox 38 + 1-u53 1 + ln 14 + divide 8 + exp 11 + 2 mul = 74
+#   sample: x beta (Gamma) or x 1/S + sum (Dirichlet)                = 1 / 2
+# evaluated on the measured trial / boost mix of each config.
+GAMMA_TRIAL_SLOTS = 88
+GAMMA_BOOST_SLOTS = 74
+GAMMA_SAMPLE_SLOTS = 1
+DIRICHLET_SAMPLE_SLOTS = 2
 
 
 def ncu_traffic(kernel_substr):
@@ -70,8 +76,8 @@ def ncu_traffic(kernel_substr):
     return best
 
 
-NCU_KERNEL = {"cfg1_gibbs": "gibbs_kernel<1, 1, 64>", "cfg2_gaussian": "fill_f32_kernel<3>",
-              "cfg2_uniform": "fill_f32_kernel<2>", "cfg3_gamma": "gamma_kernel<double>",
+NCU_KERNEL = {"cfg1_gibbs": "gibbs_kernel<1, 1, 64>", "cfg2_gaussian": "fill_kernel<float, 3, 0>",
+              "cfg2_uniform": "fill_kernel<float, 2, 0>", "cfg3_gamma": "gamma_kernel<double>",
               "cfg4_dirichlet": "dirichlet_smem_kernel<float>",
               "cfg5_gibbs": "gibbs_kernel<0, 2, 256>"}
 
@@ -311,17 +317,21 @@ def gpu_arm(args):
 
     # ---- roofline of the dominant kernel + breakdown -------------------------
     sm_hz = (clk.get("sm_max_mhz") or sm_max_cfg) * 1e6
-    issue_peak = SMS * SMSP * LANES * sm_hz            # thread-instructions / s
     pipe_peak = SMS * FP64_LANES_PER_SM * sm_hz        # fp64-pipe slots / s
-    # Gamma trial mix of cfg3, measured once (untimed) from the trials output
+    # Gamma / Dirichlet trial mixes, measured once (untimed) from the trials outputs
     wl.trials = torch.empty(wl.c3["n"], dtype=torch.uint8, device=wl.dev)
     B.brng_set_offset(wl.h3, wl.base3)
     B.brng_gamma_f64(wl.h3, wl.p3["alpha"], wl.p3["beta"], wl.o3, wl.c3["n"], wl.trials)
-    mean_trials = wl.trials.double().mean().item()
-    frac_boost = (wl.p3["alpha"] < 1).double().mean().item()
+    mix = {"cfg3_gamma": (wl.trials.double().mean().item(),
+                          (wl.p3["alpha"] < 1).double().mean().item(), GAMMA_SAMPLE_SLOTS)}
+    D4, K4 = wl.p4.shape
+    wl.trials = torch.empty(D4, K4, dtype=torch.uint8, device=wl.dev)
+    B.brng_set_offset(wl.h4, wl.base4)
+    B.brng_dirichlet_f32(wl.h4, wl.p4, D4, K4, wl.o4, wl.trials)
+    mix["cfg4_dirichlet"] = (wl.trials.double().mean().item(),
+                             (wl.p4 < 1).double().mean().item(), DIRICHLET_SAMPLE_SLOTS)
     wl.trials = None
-    gamma_instr = (mean_trials * GAMMA_TRIAL_INSTR + frac_boost * GAMMA_BOOST_INSTR
-                   + GAMMA_SAMPLE_INSTR)
+    torch.cuda.synchronize()
     bd = {}
     for n in names:
         t = per[n] * 1e-3
@@ -329,10 +339,12 @@ def gpu_arm(args):
         if n in ("cfg2_gaussian", "cfg2_uniform"):
             gbs = 12.0 * wl.samples[n] / t / 1e9
             d.update(bound="hbm", GB_per_s=round(gbs, 1), frac=round(gbs / hbm_peak, 4))
-        elif n == "cfg3_gamma":
-            a = gamma_instr * wl.samples[n] / t
-            d.update(bound="alu", frac=round(a / issue_peak, 4), mean_trials=round(mean_trials, 5),
-                     boost_frac=round(frac_boost, 4))
+        elif n in mix:
+            mt, fb, per_sample = mix[n]
+            slots = mt * GAMMA_TRIAL_SLOTS + fb * GAMMA_BOOST_SLOTS + per_sample
+            a = slots * wl.samples[n] / t
+            d.update(bound="alu", frac=round(a / pipe_peak, 4), mean_trials=round(mt, 5),
+                     boost_frac=round(fb, 4), pipe_slots_per_sample=round(slots, 2))
         elif n in ("cfg1_gibbs", "cfg5_gibbs"):
             a = GIBBS_PIPE_OPS_PER_SWEEP * (wl.samples[n] / 2) / t
             d.update(bound="alu", frac=round(a / pipe_peak, 4),

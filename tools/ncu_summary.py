@@ -83,6 +83,16 @@ def main():
           "| kernel | ms | share |", "|---|---|---|"]
     for k, t in ours:
         md.append(f"| `{k[:80]}` | {t:.4f} | {t / tot:.3%} |")
+    # per kernel: launches, mean ms per launch, share of all our kernel time
+    # (every step launches the same list, so this is also the share of a step)
+    agg = {}
+    for k, t in ours:
+        n, s = agg.get(k, (0, 0.0))
+        agg[k] = (n + 1, s + t)
+    md += ["", "## Per kernel (share of the step)", "",
+           "| kernel | launches | mean ms | share |", "|---|---|---|---|"]
+    for k, (n, s) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        md.append(f"| `{k[:80]}` | {n} | {s / n:.4f} | {s / tot:.2%} |")
     md += ["", "## Full captures", "", "| kernel | " + " | ".join(KEYS) + " | traffic_GB |",
            "|" + "---|" * (len(KEYS) + 2)]
     for m in kern:
