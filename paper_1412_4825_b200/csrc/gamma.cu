@@ -29,6 +29,7 @@ constexpr uint32_t kFull = 0xffffffffu;
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
+
 // One Marsaglia-Tsang trial (R-09) and the alpha<1 boost (R-10): the public
 // device API's (include/brng_device.cuh): binary32 decision with a binary64
 // recheck band, binary64 values.

@@ -81,12 +81,17 @@ __device__ __forceinline__ double u53_scaled(uint32_t lo, uint32_t hi) {
 // unbiased exponent of X, the bin is the top E-55 bits of 1.mantissa, all in
 // the high word; E < 56 (and X = 0) shift everything out (shift >= 21; PTX
 // shr clamps shifts >= 32 to a zero result).
-__device__ __forceinline__ uint32_t bin256_scaled(double X) {
+// Shared address of X's histogram counter: base | 4 floor(256 x), with base
+// 1024-aligned (a live chain's histogram, or the sink of a dead chain).  The
+// shift by two less yields 4 bin + 2 stray low bits, cleared by the same LOP3
+// that ORs the base in: all ALU-pipe work (no IMAD.SHL / IMAD.MOV on the
+// FMA-heavy pipe).
+__device__ __forceinline__ uint32_t bin_addr_scaled(double X, uint32_t base) {
   const uint32_t h = (uint32_t)__double2hiint(X);
-  const uint32_t sh = 1099u - (h >> 20);                    // 20 - (E - 56)
+  const uint32_t sh = 1097u - (h >> 20);
   uint32_t b;
   asm("shr.b32 %0, %1, %2;" : "=r"(b) : "r"((h & 0xFFFFFu) | 0x100000u), "r"(sh));
-  return b;
+  return (b & 0x3FCu) | base;
 }
 
 // Histogram increment at a 32-bit shared-window address (no return value).
@@ -195,8 +200,9 @@ __device__ __forceinline__ void sweeps(const GibbsArgs& a, const RoundKeys& rk, 
           q.S1X = __dadd_rn(q.S1X, q.X); q.S2X = __fma_rn(q.X, q.X, q.S2X);
           q.S1Y = __dadd_rn(q.S1Y, q.Y); q.S2Y = __fma_rn(q.Y, q.Y, q.S2Y);
           q.SXY = __fma_rn(q.X, q.Y, q.SXY);
-          // a dead chain (invalid start / padding) counts into bin 256, never read
-          hist_inc(hist_base + 4u * (q.live ? bin256_scaled(q.X) : 256u));
+          // a dead chain (invalid start / padding) counts into the sink
+          // histogram hist[256..511], never read
+          hist_inc(bin_addr_scaled(q.X, q.live ? hist_base : hist_base + 1024u));
         }
       }
       p0 += kPhiloxM0;
@@ -219,11 +225,11 @@ __global__ void __launch_bounds__(THREADS, (THREADS == kThreads ? BRNG_GIBBS_MIN
 gibbs_kernel(GibbsArgs a) {
   constexpr int kW = THREADS / 32;
   constexpr int kBinsPerThread = 256 / THREADS;
-  __shared__ uint32_t hist[257];              // [256] = sink for dead chains
+  __shared__ __align__(1024) uint32_t hist[512];   // [256..511]: sink for dead chains
   __shared__ double red[kW][8];
   const uint32_t hist_base = (uint32_t)__cvta_generic_to_shared(hist);
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int b = threadIdx.x; b < 257; b += THREADS) hist[b] = 0;
+  for (int b = threadIdx.x; b < 512; b += THREADS) hist[b] = 0;
   if (lane < 8) red[wid][lane] = 0.0;
   double bins[kBinsPerThread];                 // bins threadIdx.x + j*THREADS, accumulated
 #pragma unroll
