@@ -500,6 +500,8 @@ def e2e_run(wl, torch, B, args, allreduce, world, dist):
     steps = max(1, min(args.steps, args.e2e_steps))
     ms = timed(step_concurrent, steps)
     ms_serial = timed(step_serial, 1)
+    ms_gibbs_rows = timed(group_gibbs, 1)       # each row group alone, for the overlap
+    ms_io_rows = timed(group_io, 1)             # accounting (not part of the value)
     s0 = torch.cuda.current_stream().cuda_stream
     for h in (wl.h1, wl.h2, wl.h3, wl.h4, wl.h5):
         B.brng_set_cuda_stream(h, s0)
@@ -513,7 +515,9 @@ def e2e_run(wl, torch, B, args, allreduce, world, dist):
             "timing": "wall clock (perf_counter) between device synchronizations, max over ranks",
             "schedule": "two host threads: Gibbs rows on one CUDA stream, fill/Gamma/Dirichlet "
                         "rows (host-staged, chunk-pipelined) on a higher-priority stream",
-            "serial_ms_per_step": round(ms_serial, 3)}
+            "serial_ms_per_step": round(ms_serial, 3),
+            "gibbs_rows_alone_ms": round(ms_gibbs_rows, 3),
+            "io_rows_alone_ms": round(ms_io_rows, 3)}
 
 
 # ----------------------------------------------------------------------------

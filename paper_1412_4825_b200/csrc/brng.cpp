@@ -17,6 +17,9 @@
 
 #include <algorithm>
 #include <functional>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <limits>
 #include <new>
 #include <vector>
@@ -24,7 +27,14 @@
 #include "brng_internal.h"
 
 namespace {
-constexpr int kSlots = 2;
+// Staging slots per handle: H2D may run this many chunks ahead of D2H.  More
+// than double buffering matters when the handle's kernels share the GPU with
+// another stream's long launches: the chunks that became ready during such a
+// launch then all run back to back at its boundary (6 x 64 MB per array).
+#ifndef BRNG_STAGE_SLOTS
+#define BRNG_STAGE_SLOTS 6
+#endif
+constexpr int kSlots = BRNG_STAGE_SLOTS;
 constexpr size_t kChunkBytes = size_t(64) << 20;     // target staging chunk per array
 }  // namespace
 
@@ -38,6 +48,7 @@ struct brng_handle_s {
   unsigned long long* d_err;   // invalid-sample counter
   double* d_partials;          // Gibbs per-CTA partials
   size_t partials_cap;         // in doubles
+  double* d_totals;            // Gibbs totals scratch for host `totals` pointers
   // host-staging pipeline (created on the first host-pointer call)
   cudaStream_t s_in, s_out;
   cudaEvent_t ev_in[kSlots], ev_k[kSlots], ev_out[kSlots];
@@ -111,6 +122,16 @@ struct Arr {
   size_t slot_off = 0;        // offset of this array inside a staging slot
 };
 
+// BRNG_TRACE=1: host-staged calls report enqueue / wait times on stderr
+// (diagnostics for the host-buffer path; off by default).
+bool trace_on() {
+  static const bool on = [] {
+    const char* v = std::getenv("BRNG_TRACE");
+    return v != nullptr && v[0] == '1';
+  }();
+  return on;
+}
+
 int ensure_pipe(brng_t h, size_t slot_bytes) {
   if (!h->pipe_ready) {
     if (cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking) != cudaSuccess ||
@@ -146,7 +167,9 @@ using Launch =
 // Run a call over n_units.  All-device arrays: one direct launch on the
 // handle's stream (asynchronous).  Any host array: chunked pipeline; returns
 // after every host output is written.
-int run(brng_t h, std::vector<Arr>& arrs, uint64_t n_units, uint64_t align, const Launch& launch) {
+// max_units (0 = none) caps a chunk below the byte target.
+int run(brng_t h, std::vector<Arr>& arrs, uint64_t n_units, uint64_t align, const Launch& launch,
+        uint64_t max_units = 0) {
   bool any_host = false;
   for (auto& a : arrs) {
     a.host = a.ptr != nullptr && !is_device_ptr(a.ptr);
@@ -167,6 +190,7 @@ int run(brng_t h, std::vector<Arr>& arrs, uint64_t n_units, uint64_t align, cons
   for (auto& a : arrs)
     if (a.host) widest = std::max(widest, a.unit_bytes * a.rows);
   uint64_t chunk = std::max<uint64_t>(align, (kChunkBytes / widest) / align * align);
+  if (max_units) chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(align, max_units / align * align));
   chunk = std::min<uint64_t>(chunk, n_units);
   size_t slot = 0;
   for (auto& a : arrs)
@@ -174,6 +198,7 @@ int run(brng_t h, std::vector<Arr>& arrs, uint64_t n_units, uint64_t align, cons
       a.slot_off = slot;
       slot += (a.unit_bytes * a.rows * chunk + 255) & ~size_t(255);
     }
+  const auto t_beg = std::chrono::steady_clock::now();
   int st = ensure_pipe(h, slot);
   if (st) return st;
   // the first copies must not overtake earlier work of this handle's stream
@@ -214,8 +239,16 @@ int run(brng_t h, std::vector<Arr>& arrs, uint64_t n_units, uint64_t align, cons
     }
     if (e == cudaSuccess) e = cudaEventRecord(h->ev_out[b], h->s_out);
   }
+  const auto t_enq = std::chrono::steady_clock::now();
   cudaError_t e2 = cudaStreamSynchronize(h->s_out);
   cudaError_t e3 = cudaStreamSynchronize(h->stream);
+  if (trace_on()) {
+    const auto t_end = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[brng] staged call: %llu units, %llu chunks, enqueue %.2f ms, wait %.2f ms\n",
+                 (unsigned long long)n_units, (unsigned long long)n_chunks,
+                 std::chrono::duration<double, std::milli>(t_enq - t_beg).count(),
+                 std::chrono::duration<double, std::milli>(t_end - t_enq).count());
+  }
   if (e == cudaSuccess) e = e2;
   if (e == cudaSuccess) e = e3;
   return cuda_status(e);
@@ -344,7 +377,7 @@ int brng_create(uint64_t seed, uint64_t stream_id, brng_t* out) {
   if (!h) return BRNG_ERR_CUDA;
   h->seed = seed; h->stream_id = stream_id; h->cursor = 0;
   h->device = dev; h->num_sms = sms; h->stream = nullptr;
-  h->d_partials = nullptr; h->partials_cap = 0;
+  h->d_partials = nullptr; h->partials_cap = 0; h->d_totals = nullptr;
   h->pipe_ready = false; h->stage_cap = 0;
   if (cudaMalloc(&h->d_err, sizeof(unsigned long long)) != cudaSuccess ||
       cudaMemset(h->d_err, 0, sizeof(unsigned long long)) != cudaSuccess) {
@@ -361,6 +394,7 @@ int brng_destroy(brng_t h) {
   cudaStreamSynchronize(h->stream);
   cudaFree(h->d_err);
   if (h->d_partials) cudaFree(h->d_partials);
+  if (h->d_totals) cudaFree(h->d_totals);
   if (h->pipe_ready) {
     cudaStreamSynchronize(h->s_in);
     cudaStreamSynchronize(h->s_out);
@@ -515,16 +549,28 @@ int brng_gibbs_triangle(brng_t h, uint64_t n_chains, uint64_t n_sweeps, const do
   // device scratch that every chunk accumulates into
   double* dtot = totals;
   const bool host_tot = totals != nullptr && !is_device_ptr(totals);
-  if (host_tot && cudaMallocAsync(reinterpret_cast<void**>(&dtot), BRNG_TOTALS_LEN * 8,
-                                  h->stream) != cudaSuccess)
+  // (a handle-owned buffer, allocated once: a per-call cudaMallocAsync /
+  // cudaFreeAsync pair was measured to stall some calls by 0.3-0.6 s)
+  if (host_tot && h->d_totals == nullptr &&
+      cudaMalloc(reinterpret_cast<void**>(&h->d_totals), BRNG_TOTALS_LEN * 8) != cudaSuccess)
     return BRNG_ERR_CUDA;
+  if (host_tot) dtot = h->d_totals;
   std::vector<Arr> arrs = {{x0, 8, false},
                            {y0, 8, false},
                            {out_x, 8, true, (size_t)n_sweeps},
                            {out_y, 8, true, (size_t)n_sweeps},
                            {chain_stats, 8, true, 5},
                            {final_xy, 8, true, 2}};
-  st = run(h, arrs, n_chains, 1,
+  // Gibbs chunks: whole resident waves (no partly filled last round), two
+  // per chunk, so a chunk is a few ms of kernel: kernels of other streams
+  // (e.g. a concurrent host-staged fill) find a launch boundary that often
+  // instead of waiting behind one long-lived wave of persistent CTAs.
+#ifndef BRNG_GIBBS_CHUNK_WAVES
+#define BRNG_GIBBS_CHUNK_WAVES 2
+#endif
+  const uint64_t wave = brng::gibbs_wave_chains(ctx);
+  const uint64_t align = (BRNG_GIBBS_CHUNK_WAVES && n_chains >= wave) ? wave : 1;
+  st = run(h, arrs, n_chains, align,
            [&](uint64_t c0, uint64_t nc, const std::vector<void*>& d, bool first) {
              Ctx cc = ctx;
              cc.stream_id = ctx.stream_id + c0;
@@ -533,11 +579,11 @@ int brng_gibbs_triangle(brng_t h, uint64_t n_chains, uint64_t n_sweeps, const do
                                        static_cast<double*>(d[2]), static_cast<double*>(d[3]),
                                        static_cast<double*>(d[4]), static_cast<double*>(d[5]),
                                        dtot, h->d_partials, base, cc, !first);
-           });
+           },
+           BRNG_GIBBS_CHUNK_WAVES * wave);
   if (host_tot) {
     cudaError_t e = cudaMemcpyAsync(totals, dtot, BRNG_TOTALS_LEN * 8, cudaMemcpyDeviceToHost,
                                     h->stream);
-    cudaFreeAsync(dtot, h->stream);
     cudaError_t e2 = cudaStreamSynchronize(h->stream);
     if (!st && (e != cudaSuccess || e2 != cudaSuccess)) st = BRNG_ERR_CUDA;
   }

@@ -35,6 +35,9 @@ cudaError_t launch_dirichlet(int dtype, const void* alpha, uint64_t n_rows, uint
 // K5-K7: Gibbs chains + stats + histogram, then the fixed-order reduction.
 // partials: device scratch of at least gibbs_partials_len(...) doubles.
 size_t gibbs_partials_len(uint64_t n_chains, const Ctx& ctx);
+// Chains one resident wave of the bulk Gibbs launch holds (host-staged calls
+// cut chunks at multiples of it: no partly filled last round per chunk).
+uint64_t gibbs_wave_chains(const Ctx& ctx);
 cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
                          const double* y0, uint64_t burn_in, double* out_x, double* out_y,
                          double* chain_stats, double* final_xy, double* totals,

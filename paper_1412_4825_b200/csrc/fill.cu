@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kThreads) fill_kernel(const __grid_constant__ 
     for (int b = 0; b < kBPT; ++b) {
       const uint64_t j = j0 + b * stride;
       if (j >= nblk) break;
-      const uint4 w = philox_block_rk(a.base + j, a.stream, a.rk);
+      const uint4 w = philox_block_rk(a.base + j, a.rk);
       T s[S];
       std_block<DIST>(w, s);
       const uint64_t i0 = j * S;
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kThreads) raw_u32_kernel(const __grid_constant
   const uint64_t nblk = (a.n + 3) >> 2;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   for (uint64_t j = (uint64_t)blockIdx.x * kThreads + threadIdx.x; j < nblk; j += stride) {
-    const uint4 w = philox_block_rk(a.base + j, a.stream, a.rk);
+    const uint4 w = philox_block_rk(a.base + j, a.rk);
     const uint64_t i0 = j << 2;
     if (a.vec && i0 + 4 <= a.n) {
       __stcs(reinterpret_cast<uint4*>(a.out) + j, w);
@@ -258,7 +258,7 @@ cudaError_t run_dist(const T* p0, const T* p1, T* out, uint64_t n, uint64_t base
                      const Ctx& ctx, const double* scalars) {
   constexpr int S = spb<T, DIST>();
   const uintptr_t vb = sizeof(T) * S;
-  FillArgs<T> a{p0, p1, out, n, base, ctx.stream_id, make_round_keys(ctx.k0, ctx.k1),
+  FillArgs<T> a{p0, p1, out, n, base, ctx.stream_id, make_round_keys(ctx.k0, ctx.k1, ctx.stream_id),
                 aligned(p0, vb) && aligned(p1, vb) && aligned(out, vb), ctx.err, T(0), T(0)};
   const unsigned g = grid_for((n + S - 1) / S, ctx);
   if (scalars) {
@@ -298,7 +298,7 @@ cudaError_t launch_fill(int dist, int dtype, const void* p0, const void* p1, voi
                         uint64_t n, uint64_t base, const Ctx& ctx, const double* scalars) {
   if (dist == kRaw) {
     FillArgs<uint32_t> a{nullptr, nullptr, static_cast<uint32_t*>(out), n, base, ctx.stream_id,
-                         make_round_keys(ctx.k0, ctx.k1), aligned(out, 16), ctx.err};
+                         make_round_keys(ctx.k0, ctx.k1, ctx.stream_id), aligned(out, 16), ctx.err};
     raw_u32_kernel<<<grid_for((n + 3) >> 2, ctx), kThreads, 0, ctx.stream>>>(a);
     return cudaGetLastError();
   }

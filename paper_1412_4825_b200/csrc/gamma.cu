@@ -36,6 +36,11 @@ __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000
 using brng_dev::mt_boost;
 using brng_dev::mt_trial;
 
+// Lookup tables of the trial/boost math: read through the read-only path
+// (GlobalTables).  Staging them in shared memory was measured slower
+// (cfg3 0.929 -> 0.987 ms: random 16-B LDS bank conflicts).
+using Tables = brng_dev::dm::GlobalTables;
+
 // alpha<1 boost work item, parked in a per-warp shared-memory queue so that
 // boosts run as full warps instead of as a divergent branch (36% of cfg3's
 // samples, 91% of cfg4's).
@@ -54,7 +59,7 @@ constexpr int kBoostCap = 64;
 // iteration, queued or not) never changes it.
 template <typename Load, typename Sink>
 __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t base,
-                                         uint64_t stream, const RoundKeys& rk, Load load,
+                                         const RoundKeys& rk, const Tables& tb, Load load,
                                          Sink sink, uint32_t& nbad, BoostItem* q) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
@@ -76,8 +81,8 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
     if (lane < n) {
       const BoostItem it = q[qn - n + lane];
       const uint64_t ii = it.i_t & 0x00FFFFFFFFFFFFFFull;
-      const uint4 wb = philox_block_rk(base + (uint64_t)kStride * ii, stream, rk);
-      const double gb = mt_boost(wb, it.g, it.alpha);
+      const uint4 wb = philox_block_rk(base + (uint64_t)kStride * ii, rk);
+      const double gb = mt_boost(wb, it.g, it.alpha, tb);
       sink(ii, gb * it.beta, (uint32_t)(it.i_t >> 56));
     }
     qn -= n;
@@ -88,9 +93,9 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
     bool done = false, boost = false;
     double g = 0.0;
     if (active) {
-      const uint4 w = philox_block_rk(base + (uint64_t)kStride * i + t, stream, rk);
+      const uint4 w = philox_block_rk(base + (uint64_t)kStride * i + t, rk);
       const bool valid = isfinite(alpha) && isfinite(beta) && alpha > 0.0 && beta > 0.0;
-      const bool acc = mt_trial(w, alpha, d, g);
+      const bool acc = mt_trial(w, alpha, d, g, tb);
       if (!valid) {
         done = true; t = 0; ++nbad;
       } else if (acc) {
@@ -138,6 +143,7 @@ template <typename T>
 #endif
 __global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(const __grid_constant__ GammaArgs<T> a) {
   __shared__ BoostItem qs[kThreads / 32][kBoostCap];
+  const Tables tb{};
   BoostItem* q = qs[threadIdx.x >> 5];
   const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   const uint64_t n_warps = ((uint64_t)gridDim.x * kThreads) >> 5;
@@ -145,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(const 
   for (uint64_t beg = warp * kChunk; beg < a.n; beg += n_warps * kChunk) {
     const uint64_t end = beg + kChunk < a.n ? beg + kChunk : a.n;
     mt_queue(
-        beg, end, a.base, a.stream, a.rk,
+        beg, end, a.base, a.rk, tb,
         [&](uint64_t i, double& al, double& be) {
           al = (double)__ldg(a.alpha + i);
           be = (double)__ldg(a.beta + i);
@@ -185,6 +191,7 @@ template <typename T>
 __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __grid_constant__ DirArgs<T> a) {
   extern __shared__ double gsm[];
   __shared__ BoostItem qs[kDirThreads / 32][kBoostCap];
+  const Tables tb{};
   BoostItem* q = qs[threadIdx.x >> 5];
   const uint32_t lane = threadIdx.x & 31;
   double* g_row = gsm + (threadIdx.x >> 5) * a.k;
@@ -194,7 +201,7 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __gri
   for (uint64_t row = warp; row < a.n_rows; row += n_warps) {
     const uint64_t beg = row * a.k;
     mt_queue(
-        beg, beg + a.k, a.base, a.stream, a.rk,
+        beg, beg + a.k, a.base, a.rk, tb,
         [&](uint64_t i, double& al, double& be) {
           al = (double)__ldg(a.alpha + i);
           be = 1.0;
@@ -220,6 +227,7 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __gri
 template <typename T>
 __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(const __grid_constant__ DirArgs<T> a) {
   __shared__ BoostItem qs[kDirThreads / 32][kBoostCap];
+  const Tables tb{};
   BoostItem* q = qs[threadIdx.x >> 5];
   const uint64_t warp = ((uint64_t)blockIdx.x * kDirThreads + threadIdx.x) >> 5;
   const uint64_t n_warps = ((uint64_t)gridDim.x * kDirThreads) >> 5;
@@ -231,11 +239,11 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(const __gr
       be = 1.0;
     };
     double s = 0.0;
-    mt_queue(beg, beg + a.k, a.base, a.stream, a.rk, load,
+    mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
              [&](uint64_t, double v, uint32_t) { s += v; }, nbad, q);
     s = warp_sum(s);
     const double inv = 1.0 / s;
-    mt_queue(beg, beg + a.k, a.base, a.stream, a.rk, load,
+    mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
              [&](uint64_t i, double v, uint32_t t) {
                a.out[i] = (T)(v * inv);
                if (a.trials) a.trials[i] = (uint8_t)t;
@@ -249,7 +257,7 @@ template <typename T>
 cudaError_t gamma_typed(const T* alpha, const T* beta, T* out, uint8_t* trials, uint64_t n,
                         uint64_t base, const Ctx& ctx) {
   GammaArgs<T> a{alpha, beta, out, trials, n, base, ctx.stream_id,
-                   make_round_keys(ctx.k0, ctx.k1), ctx.err};
+                   make_round_keys(ctx.k0, ctx.k1, ctx.stream_id), ctx.err};
   const uint64_t warps_needed = (n + kChunk - 1) / kChunk;
   const uint64_t ctas_needed = (warps_needed + (kThreads / 32) - 1) / (kThreads / 32);
   const uint64_t cap = (uint64_t)ctx.num_sms * 8;  // one full-occupancy wave
@@ -262,7 +270,7 @@ template <typename T>
 cudaError_t dirichlet_typed(const T* alpha, uint64_t n_rows, uint64_t k, T* out,
                             uint8_t* trials, uint64_t base, const Ctx& ctx) {
   DirArgs<T> a{alpha, out, trials, n_rows, k, base, ctx.stream_id,
-                 make_round_keys(ctx.k0, ctx.k1), ctx.err};
+                 make_round_keys(ctx.k0, ctx.k1, ctx.stream_id), ctx.err};
   const uint64_t ctas_needed = (n_rows + 3) / 4;
   if (k <= kDirSmemK) {
     const size_t smem = (size_t)4 * k * sizeof(double);

@@ -383,6 +383,10 @@ inline Shape grid_shape(uint64_t n_chains, const Ctx& ctx) {
 
 }  // namespace
 
+uint64_t gibbs_wave_chains(const Ctx& ctx) {
+  return (uint64_t)ctx.num_sms * ctas_per_sm_bulk() * kThreads * kCPT;
+}
+
 // Enough for any launch shape (one resident wave), so chunked calls that
 // launch different grids can share the handle's scratch.
 size_t gibbs_partials_len(uint64_t /*n_chains*/, const Ctx& ctx) {
