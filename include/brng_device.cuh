@@ -115,6 +115,15 @@ static __constant__ double kC[kNumConst] = {
     6755399441055744.0,              // 1.5 * 2^52: round-to-integer shifter
     0.375, 1.0 / 3.0,
 };
+// Where the lookup tables are read from.  GlobalTables: the __device__ arrays
+// through the read-only path (any user kernel).  A kernel may instead stage
+// the same arrays elsewhere (e.g. shared memory) behind the same interface:
+// same values, so the same results bit for bit.
+struct GlobalTables {
+  __device__ __forceinline__ double2 ln(int j) const { return __ldg(&tab::kLn[j]); }
+  __device__ __forceinline__ double2 cs(uint32_t j) const { return __ldg(&tab::kCos[j]); }
+  __device__ __forceinline__ double exp2(int j) const { return __ldg(&tab::kExp2[j]); }
+};
 // exact binary64 of a 32-bit signed integer without the I2F pipe
 __device__ __forceinline__ double i2d(int v) {
   return __hiloint2double(0x43300000, v ^ (int)0x80000000) - kC[kI2dBias];
@@ -133,12 +142,13 @@ __device__ __forceinline__ double one_minus_u53(uint32_t lo, uint32_t hi) {
 // 0.0056); ln x = e ln2 - ln c_j + log1p(r), log1p by its Taylor series to
 // r^7.  c_0 = 1 and ln c_0 = 0, so for x near 1 the result is log1p(x-1)
 // to ~1 ulp relative.
-__device__ __forceinline__ double ln_pos(double x) {
+template <class Tab = GlobalTables>
+__device__ __forceinline__ double ln_pos(double x, const Tab& tb = Tab()) {
   const int hx = __double2hiint(x);
   const int e = (hx - 0x3FE6A09E) >> 20;
   const double m = __hiloint2double(hx - e * (1 << 20), __double2loint(x));
   const int j = __double2loint(fma(m, 128.0, kC[kRndM128]));
-  const double2 ct = __ldg(&tab::kLn[j + tab::kLnOff]);
+  const double2 ct = tb.ln(j + tab::kLnOff);
   const double r = fma(m, ct.x, -1.0);
   double q = fma(r, kC[kL7], kC[kL6]);
   q = fma(r, q, kC[kL5]);
@@ -152,10 +162,11 @@ __device__ __forceinline__ double ln_pos(double x) {
 // cos(2 pi w 2^-32): j = round(w / 2^24) mod 256, b = 2 pi (w - j 2^24) 2^-32
 // (|b| <= pi/256); cos(a_j + b) = C_j cos b - S_j sin b with Taylor cos b - 1
 // to b^6 and sin b to b^7.  Absolute error ~1e-16.
-__device__ __forceinline__ double cos2pi_u32(uint32_t w) {
+template <class Tab = GlobalTables>
+__device__ __forceinline__ double cos2pi_u32(uint32_t w, const Tab& tb = Tab()) {
   const uint32_t j = (w + 0x800000u) >> 24;
   const double b = i2d((int)(w - (j << 24))) * kC[kTwoPi32];
-  const double2 cs = __ldg(&tab::kCos[j]);
+  const double2 cs = tb.cs(j);
   const double b2 = b * b;
   const double s = fma(b2 * b, fma(b2, fma(b2, kC[kS7], kC[kS5]), kC[kS3]), b);
   const double cm1 = b2 * fma(b2, fma(b2, kC[kC6], kC[kC4]), -0.5);
@@ -164,7 +175,8 @@ __device__ __forceinline__ double cos2pi_u32(uint32_t w) {
 // e^y for finite y <= 0: k = round(64 y / ln 2), r = y - k ln2/64 (|r| <=
 // 0.0055, Cody-Waite), e^y = 2^(k>>6) 2^((k&63)/64) e^r, e^r - 1 by Taylor
 // to r^6.  y < -700 (result near/below the normal range) takes libdevice.
-__device__ __forceinline__ double exp_nonpos(double y) {
+template <class Tab = GlobalTables>
+__device__ __forceinline__ double exp_nonpos(double y, const Tab& tb = Tab()) {
   if (y < -700.0) return exp(y);
   const double t = fma(y, kC[kInvLn2x64], kC[kRnd]);
   const int k = __double2loint(t);
@@ -176,7 +188,7 @@ __device__ __forceinline__ double exp_nonpos(double y) {
   q = fma(r, q, kC[kE3]);
   q = fma(r, q, 0.5);
   const double p = fma(r * r, q, r);
-  const double T = __ldg(&tab::kExp2[k & 63]);
+  const double T = tb.exp2(k & 63);
   const double v = fma(T, p, T);
   return __hiloint2double(__double2hiint(v) + (k >> 6) * (1 << 20), __double2loint(v));
 }
@@ -261,9 +273,11 @@ __device__ __forceinline__ bool mt_exact(double z, double d, double v, uint32_t 
 // (~0.1% of trials) re-run the exact binary64 test in the contract's
 // operation order.  Decisions are therefore the binary64 contract's.
 // d is returned; alpha is consumed only after z (hides its load latency).
-__device__ __forceinline__ bool mt_trial(uint4 w, double alpha, double& d, double& g) {
-  const double L = dm::ln_pos(dm::one_minus_u53(w.x, w.y));
-  const double z = __dmul_rn(dm::sqrt_nonneg(-2.0 * L), dm::cos2pi_u32(w.z));
+template <class Tab = dm::GlobalTables>
+__device__ __forceinline__ bool mt_trial(uint4 w, double alpha, double& d, double& g,
+                                         const Tab& tb = Tab()) {
+  const double L = dm::ln_pos(dm::one_minus_u53(w.x, w.y), tb);
+  const double z = __dmul_rn(dm::sqrt_nonneg(-2.0 * L), dm::cos2pi_u32(w.z, tb));
   double c;
   mt_consts(alpha, d, c);
   const double cz = __dmul_rn(c, z);
@@ -276,8 +290,10 @@ __device__ __forceinline__ bool mt_trial(uint4 w, double alpha, double& d, doubl
   return mt_exact(z, d, v, w.w);
 }
 // alpha < 1 boost (R-10): g * exp(ln(1-u53(w0,w1)) / alpha) from block 256 i.
-__device__ __forceinline__ double mt_boost(uint4 wb, double g, double alpha) {
-  return g * dm::exp_nonpos(dm::ln_pos(dm::one_minus_u53(wb.x, wb.y)) / alpha);
+template <class Tab = dm::GlobalTables>
+__device__ __forceinline__ double mt_boost(uint4 wb, double g, double alpha,
+                                           const Tab& tb = Tab()) {
+  return g * dm::exp_nonpos(dm::ln_pos(dm::one_minus_u53(wb.x, wb.y), tb) / alpha, tb);
 }
 
 // ---- per-sample getters: value of sample i of the bulk call at cursor base --------
