@@ -1,6 +1,6 @@
 """Time build variants of libbrng (tools/variants/*.so) on one kernel.
 
-usage: python tools/variant_time.py gibbs|gamma|dirichlet|gaussian|uniform [lib ...]
+usage: python tools/variant_time.py gibbs|gibbs1|gamma|gamma32|dirichlet|gaussian|uniform [lib ...]
 Each variant runs in its own process (BRNG_LIB=...); prints ms and a hash of
 the outputs so variants can be checked for identical results.
 """
@@ -41,6 +41,16 @@ elif what == "gibbs":
         B.brng_set_offset(h, 0)
         B.brng_gibbs_triangle(h, nc, ns, None, None, 0, None, None, st, fx, tot)
     outs = [st, fx, tot[16:]]
+elif what == "gamma32":
+    n = 1 << 26
+    p = W.cfg3_params(n, seed=11, device=dev)
+    a32, b32 = p["alpha"].float(), p["beta"].float()
+    o = torch.empty(n, dtype=torch.float32, device=dev)
+    h = B.brng_create(11, 0); B.brng_set_cuda_stream(h, s)
+    def run():
+        B.brng_set_offset(h, 0)
+        B.brng_gamma_f32(h, a32, b32, o, n, None)
+    outs = [o]
 elif what == "gamma":
     n = 1 << 26
     p = W.cfg3_params(n, seed=11, device=dev)
