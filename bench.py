@@ -46,6 +46,12 @@ SMS, SMSP, LANES = 148, 4, 32
 # 5 statistics) = 17*2 + 9 = 43 fp64-pipe slots; peak = 64 x 148 x f_sm.
 GIBBS_PIPE_OPS_PER_SWEEP = 43
 FP64_LANES_PER_SM = 64
+# cfg1 (1024 chains) is LATENCY-bound: a chain's sweeps are serial and each
+# sweep's critical path is 4 dependent fp64 ops (fma, mul, fma, mul) at the
+# measured 8.1-cycle dependent latency (tools/ulat.cu, profiles/) = 32.1
+# cycles/sweep; floor = n_sweeps x 32.1 / f_sm for any number of chains that
+# fits one wave.
+GIBBS_SWEEP_LATENCY_CYC = 32.1
 # Gamma / Dirichlet roofline (DESIGN.md §7 K3): the same FMA-heavy pipe as
 # Gibbs.  Algorithmic slots of the method as implemented (fp64 ops + 2 per
 # IMAD.WIDE), counted from the kernel's arithmetic:
@@ -76,7 +82,7 @@ def ncu_traffic(kernel_substr):
     return best
 
 
-NCU_KERNEL = {"cfg1_gibbs": "gibbs_kernel<1, 1, 64>", "cfg2_gaussian": "fill_kernel<float, 3, 0>",
+NCU_KERNEL = {"cfg1_gibbs": "gibbs_warp_kernel<1>", "cfg2_gaussian": "fill_kernel<float, 3, 0>",
               "cfg2_uniform": "fill_kernel<float, 2, 0>", "cfg3_gamma": "gamma_kernel<double>",
               "cfg4_dirichlet": "dirichlet_smem_kernel<float>",
               "cfg5_gibbs": "gibbs_kernel<0, 2, 256>"}
@@ -345,7 +351,12 @@ def gpu_arm(args):
             a = slots * wl.samples[n] / t
             d.update(bound="alu", frac=round(a / pipe_peak, 4), mean_trials=round(mt, 5),
                      boost_frac=round(fb, 4), pipe_slots_per_sample=round(slots, 2))
-        elif n in ("cfg1_gibbs", "cfg5_gibbs"):
+        elif n == "cfg1_gibbs":
+            floor_s = wl.c1["n_sweeps"] * GIBBS_SWEEP_LATENCY_CYC / sm_hz
+            d.update(bound="latency", frac=round(floor_s / t, 4),
+                     floor_us=round(floor_s * 1e6, 2),
+                     Gsweeps_per_s=round(wl.samples[n] / 2 / t / 1e9, 3))
+        elif n == "cfg5_gibbs":
             a = GIBBS_PIPE_OPS_PER_SWEEP * (wl.samples[n] / 2) / t
             d.update(bound="alu", frac=round(a / pipe_peak, 4),
                      Gsweeps_per_s=round(wl.samples[n] / 2 / t / 1e9, 3))

@@ -340,6 +340,154 @@ __global__ void __launch_bounds__(kTot) reduce_partials_kernel(const double* par
 constexpr int kSmallThreads = 64;
 constexpr int kSmallCPT = 1;
 
+// ---- latency mode: one WARP per chain (small chain counts, e.g. cfg1) ------------
+// With few chains a thread-per-chain launch leaves the GPU nearly empty and
+// each thread walks its 1000+ sweeps serially (Philox + update per sweep).
+// Here the 32 lanes of a warp compute the Philox blocks of 32 consecutive
+// sweeps of ONE chain in parallel (the blocks do not depend on the state),
+// then every lane runs the serial update x = (1-y) u, y = (1-x) u' over those
+// 32 sweeps with the uniforms broadcast by shuffles (same arithmetic, same
+// order: bit-identical samples and statistics).  Lane j keeps sweep j's
+// (x, y) for the histogram and the stores.  The critical path is the 4
+// dependent fp64 ops of a sweep; everything else is off it.
+constexpr int kLatThreads = 128;                 // 4 warps = 4 chains per CTA
+constexpr int kLatW = kLatThreads / 32;
+
+// All 10 rounds (no per-chain hoisting: 32 sweeps per lane-block here).
+__device__ __forceinline__ uint4 gibbs_block(uint64_t pos, uint64_t stream, const GibbsArgs& a) {
+  uint4 c = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), (uint32_t)stream,
+                       (uint32_t)(stream >> 32));
+#pragma unroll
+  for (int r = 0; r < 10; ++r) c = philox_round(c, a.rk0[r], a.rk1[r]);
+  return c;
+}
+
+struct WarpChain {
+  double X, Y, S1X, S2X, S1Y, S2Y, SXY;
+};
+
+// Serial update of sweeps s0 .. s0+n-1 (n = 32 unrolled when FULL).  The
+// uniforms of sweep j come from the warp's shared row u[j] (one broadcast
+// LDS.128 per sweep, issued ahead of the dependent chain); lane 0 records
+// sweep j's scaled (X, Y) in xy[j].  STATS: 1 all sweeps, 2 sweeps >= burn_in.
+// (Only the full, all-statistics batch is unrolled: the other cases are rare
+// and a second unrolled copy doubles the loop's instruction footprint.)
+template <int STATS, bool FULL>
+__device__ __forceinline__ void warp_steps(WarpChain& q, const double2* u, double2* xy,
+                                           bool lane0, uint32_t nb, uint32_t s0,
+                                           uint32_t burn_in) {
+  const int n = FULL ? 32 : (int)nb;
+  double2 un = u[0];                  // one sweep of lookahead on the LDS
+#pragma unroll (FULL ? 32 : 1)
+  for (int j = 0; j < n; ++j) {
+    const double2 uj = un;
+    if (j + 1 < n) un = u[j + 1];
+    q.X = __dmul_rn(__fma_rn(q.Y, -kInvScale, 1.0), uj.x);
+    q.Y = __dmul_rn(__fma_rn(q.X, -kInvScale, 1.0), uj.y);
+    if (STATS == 1 || (STATS == 2 && s0 + (uint32_t)j >= burn_in)) {
+      q.S1X = __dadd_rn(q.S1X, q.X); q.S2X = __fma_rn(q.X, q.X, q.S2X);
+      q.S1Y = __dadd_rn(q.S1Y, q.Y); q.S2Y = __fma_rn(q.Y, q.Y, q.S2Y);
+      q.SXY = __fma_rn(q.X, q.Y, q.SXY);
+    }
+    if (lane0) xy[j] = make_double2(q.X, q.Y);
+  }
+}
+
+template <bool STORE>
+__global__ void __launch_bounds__(kLatThreads) gibbs_warp_kernel(GibbsArgs a) {
+  __shared__ __align__(1024) uint32_t hist[512];   // [256..511]: sink for dead chains
+  __shared__ double red[kLatW][8];
+  __shared__ double2 su[kLatW][32], sxy[kLatW][32];   // per warp: uniforms, states
+  const uint32_t hist_base = (uint32_t)__cvta_generic_to_shared(hist);
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double2* const u = su[wid];
+  double2* const xy = sxy[wid];
+  const bool lane0 = lane == 0;
+  for (int b = threadIdx.x; b < 512; b += kLatThreads) hist[b] = 0;
+  if (lane < 8) red[wid][lane] = 0.0;
+  uint32_t nbad = 0;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  const double n = (double)(a.n_sweeps - a.burn_in);
+  const double nm1 = __dsub_rn(n, 1.0);
+  __syncthreads();
+  const uint64_t stride = (uint64_t)gridDim.x * kLatW;
+  for (uint64_t c = (uint64_t)blockIdx.x * kLatW + wid; c < a.n_chains; c += stride) {
+    const double x0 = a.x0 ? a.x0[c] : 0.5;
+    const double y0 = a.y0 ? a.y0[c] : 0.5;
+    const bool live = (y0 >= 0.0) && (y0 <= 1.0);
+    nbad += (lane == 0 && !live);
+    WarpChain q;
+    q.X = __dmul_rn(x0, kScale);
+    q.Y = __dmul_rn(live ? y0 : qnan, kScale);
+    q.S1X = q.S2X = q.S1Y = q.S2Y = q.SXY = 0.0;
+    const uint64_t stream = a.stream_id + c;
+    const uint32_t hb = live ? hist_base : hist_base + 1024u;
+    // the Philox blocks of batch b+1 are computed while batch b's serial
+    // updates run (independent work the scheduler interleaves)
+    uint4 w = gibbs_block(a.base + lane, stream, a);
+    for (uint32_t s0 = 0; s0 < a.n_sweeps; s0 += 32) {
+      const uint32_t nb = a.n_sweeps - s0 < 32u ? a.n_sweeps - s0 : 32u;
+      __syncwarp();
+      u[lane] = make_double2(u53_scaled(w.x, w.y), u53_scaled(w.z, w.w));
+      __syncwarp();
+      if (s0 + 32 < a.n_sweeps) w = gibbs_block(a.base + s0 + 32 + lane, stream, a);
+      if (nb == 32 && s0 >= a.burn_in)
+        warp_steps<1, true>(q, u, xy, lane0, nb, s0, a.burn_in);
+      else
+        warp_steps<2, false>(q, u, xy, lane0, nb, s0, a.burn_in);
+      __syncwarp();
+      if (lane < nb) {
+        const double2 st = xy[lane];
+        const double myX = st.x, myY = st.y;
+        const uint32_t s = s0 + lane;
+        if (s >= a.burn_in) hist_inc(bin_addr_scaled(myX, hb));
+        if (STORE && live) {
+          if (a.out_x) a.out_x[(uint64_t)s * a.n_chains + c] = __dmul_rn(myX, kInvScale);
+          if (a.out_y) a.out_y[(uint64_t)s * a.n_chains + c] = __dmul_rn(myY, kInvScale);
+        }
+      }
+    }
+    // per-chain statistics (every lane holds them; lane 0 writes)
+    const double s1x = __dmul_rn(q.S1X, kInvScale), s1y = __dmul_rn(q.S1Y, kInvScale);
+    const double s2x = __dmul_rn(q.S2X, kInvScale2), s2y = __dmul_rn(q.S2Y, kInvScale2);
+    const double sxy = __dmul_rn(q.SXY, kInvScale2);
+    const double mx = __ddiv_rn(s1x, n), my = __ddiv_rn(s1y, n);
+    const double vx = __ddiv_rn(__dsub_rn(s2x, __dmul_rn(s1x, mx)), nm1);
+    const double vy = __ddiv_rn(__dsub_rn(s2y, __dmul_rn(s1y, my)), nm1);
+    const double cxy = __ddiv_rn(__dsub_rn(sxy, __dmul_rn(s1x, my)), nm1);
+    if (lane == 0) {
+      if (a.chain_stats) {
+        a.chain_stats[0 * a.n_chains + c] = mx;
+        a.chain_stats[1 * a.n_chains + c] = vx;
+        a.chain_stats[2 * a.n_chains + c] = my;
+        a.chain_stats[3 * a.n_chains + c] = vy;
+        a.chain_stats[4 * a.n_chains + c] = cxy;
+      }
+      if (a.final_xy) {
+        a.final_xy[c] = __dmul_rn(q.X, kInvScale);
+        a.final_xy[a.n_chains + c] = __dmul_rn(q.Y, kInvScale);
+      }
+      red[wid][0] += mx; red[wid][1] += vx; red[wid][2] += mx * mx; red[wid][3] += my;
+      red[wid][4] += vy; red[wid][5] += my * my; red[wid][6] += cxy; red[wid][7] += mx * my;
+    }
+    if (STORE && !live)                 // invalid start: NaN samples (oracle semantics)
+      for (uint32_t s = lane; s < a.n_sweeps; s += 32) {
+        if (a.out_x) a.out_x[(uint64_t)s * a.n_chains + c] = qnan;
+        if (a.out_y) a.out_y[(uint64_t)s * a.n_chains + c] = qnan;
+      }
+  }
+  __syncthreads();
+  double* part = a.partials + (uint64_t)blockIdx.x * kTot;
+  if (threadIdx.x < 8) {
+    double v = 0.0;
+    for (int w = 0; w < kLatW; ++w) v += red[w][threadIdx.x];
+    part[threadIdx.x] = v;
+  }
+  for (int b = threadIdx.x; b < 256; b += kLatThreads) part[kHdr + b] = (double)hist[b];
+  flush_errors(a.err, nbad);
+}
+
+
 template <typename K>
 int occupancy(K kernel, int threads) {
   int v = 0;
@@ -356,6 +504,16 @@ int ctas_per_sm_small() {
   static int cached = occupancy(gibbs_kernel<true, kSmallCPT, kSmallThreads>, kSmallThreads);
   return cached;
 }
+int ctas_per_sm_lat() {
+  static int cached = occupancy(gibbs_warp_kernel<true>, kLatThreads);
+  return cached;
+}
+// Latency mode (one warp per chain) for chain counts up to this many per SM:
+// below it a warp per chain finishes sooner than a thread per chain (cfg1:
+// 1024 chains).
+#ifndef BRNG_GIBBS_LAT_PER_SM
+#define BRNG_GIBBS_LAT_PER_SM 32
+#endif
 
 // Launch shape: `threads` x `cpt` chains per CTA per round, one resident wave
 // of CTAs; each thread runs `rounds` rounds so chains divide evenly.
@@ -390,7 +548,8 @@ uint64_t gibbs_wave_chains(const Ctx& ctx) {
 // Enough for any launch shape (one resident wave), so chunked calls that
 // launch different grids can share the handle's scratch.
 size_t gibbs_partials_len(uint64_t /*n_chains*/, const Ctx& ctx) {
-  const int c = ctas_per_sm_bulk() > ctas_per_sm_small() ? ctas_per_sm_bulk() : ctas_per_sm_small();
+  int c = ctas_per_sm_bulk() > ctas_per_sm_small() ? ctas_per_sm_bulk() : ctas_per_sm_small();
+  if (ctas_per_sm_lat() > c) c = ctas_per_sm_lat();
   return (size_t)ctx.num_sms * c * kTot;
 }
 
@@ -411,7 +570,16 @@ cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
   a.x0 = x0; a.y0 = y0; a.out_x = out_x; a.out_y = out_y; a.chain_stats = chain_stats;
   a.final_xy = final_xy; a.partials = partials; a.err = ctx.err;
   const bool store = out_x != nullptr || out_y != nullptr;
-  if (sh.small) {
+  unsigned n_parts = grid;
+  if (n_chains <= (uint64_t)ctx.num_sms * BRNG_GIBBS_LAT_PER_SM) {
+    const uint64_t want = (n_chains + kLatW - 1) / kLatW;
+    const uint64_t cap = (uint64_t)ctx.num_sms * ctas_per_sm_lat();
+    n_parts = (unsigned)(want < cap ? (want ? want : 1) : cap);
+    if (store)
+      gibbs_warp_kernel<true><<<n_parts, kLatThreads, 0, ctx.stream>>>(a);
+    else
+      gibbs_warp_kernel<false><<<n_parts, kLatThreads, 0, ctx.stream>>>(a);
+  } else if (sh.small) {
     if (store)
       gibbs_kernel<true, kSmallCPT, kSmallThreads><<<grid, kSmallThreads, 0, ctx.stream>>>(a);
     else
@@ -425,7 +593,7 @@ cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || totals == nullptr) return e;
   reduce_partials_kernel<<<1, kTot, 0, ctx.stream>>>(
-      partials, grid, totals, (double)n_chains, (double)n_chains * (double)(n_sweeps - burn_in),
+      partials, n_parts, totals, (double)n_chains, (double)n_chains * (double)(n_sweeps - burn_in),
       accumulate ? 1 : 0);
   return cudaGetLastError();
 }

@@ -154,3 +154,28 @@ def test_host_pipeline_multi_chunk_gibbs():
     assert np.array_equal(st, g["chain_stats"]) and np.array_equal(fx, g["final_xy"])
     assert np.array_equal(tot[HDR:], g["totals"][HDR:])
     np.testing.assert_allclose(tot[:HDR], g["totals"][:HDR], rtol=1e-12)
+
+
+def test_launch_shapes_agree_across_the_latency_threshold():
+    """Three launch shapes serve different chain counts (warp per chain up to
+    32 chains per SM, thread per chain below half a bulk wave, two chains per
+    thread above).  A chain's samples, statistics and final state must not
+    depend on which one ran it: chains 0..n-1 of a run just above the
+    warp-per-chain threshold equal the same chains of a run just below it,
+    and both equal the oracle on sampled chains; histograms are exact."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    thr = 32 * sms                          # BRNG_GIBBS_LAT_PER_SM (gibbs.cu)
+    ns, burn = 40, 3
+    lo = _run(42, 5, 1000, thr, ns, burn)            # warp per chain
+    hi = _run(42, 5, 1000, thr + 37, ns, burn)       # thread per chain
+    for k in ("out_x", "out_y"):
+        assert np.array_equal(lo[k], hi[k][:, :thr]), k
+    assert np.array_equal(lo["chain_stats"], hi["chain_stats"][:, :thr])
+    assert np.array_equal(lo["final_xy"], hi["final_xy"][:, :thr])
+    for c in (0, 1, thr // 2, thr - 1):
+        r = oracle.gibbs_triangle(42, 5 + c, 1000, 1, ns, burn_in=burn)
+        assert np.array_equal(lo["out_x"][:, c], r["out_x"][:, 0])
+        assert np.array_equal(lo["chain_stats"][:, c], r["chain_stats"][:, 0])
+    # histogram of the first thr chains is the same whichever kernel counted it
+    extra = _run(42, 5 + thr, 1000, 37, ns, burn)
+    assert np.array_equal(lo["totals"][HDR:] + extra["totals"][HDR:], hi["totals"][HDR:])
