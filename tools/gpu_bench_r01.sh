@@ -1,10 +1,12 @@
+# Round-1 measurement bundle (run under gpurun from the repo root):
+#   bench line, ncu launch list of one bench step, --set full capture of each kernel.
 set -x
-python bench.py > gpurun_out/bench_r01c.json 2> gpurun_out/bench_r01c.err
+python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
 echo "bench rc=$?"
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_r01c.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_list.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_final.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_list.log 2>&1
 echo "ncu list rc=$?"
 for k in gamma dirichlet gaussian uniform gibbs1; do
-  ncu --set full --import-source on --clock-control none -s 1 -c 1 -k regex:'gamma_kernel|dirichlet|fill_|gibbs_kernel' -o gpurun_out/full_$k python tools/run_kernel.py $k > gpurun_out/ncu_$k.log 2>&1
+  ncu --set full --import-source on --clock-control none -s 1 -c 1 -k regex:'gamma_kernel|dirichlet|fill_|gibbs_' -o gpurun_out/full_$k python tools/run_kernel.py $k > gpurun_out/ncu_$k.log 2>&1
 done
 ncu --set full --import-source on --clock-control none -c 1 -k regex:'gibbs_kernel' -o gpurun_out/full_gibbs python tools/run_kernel.py gibbs > gpurun_out/ncu_gibbs.log 2>&1
 echo done

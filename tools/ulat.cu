@@ -62,6 +62,28 @@ __global__ void k_lat(double* out, long long* cyc, double seed, int mode) {
       a6 = __fmaf_rn(a6, 0.999f, 1e-7f); a7 = __fmaf_rn(a7, 0.999f, 1e-7f);
     }
     x = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  } else if (mode == 11 || mode == 12) {  // sweep, u from LDS (lookahead 4), state recorded per step
+    __shared__ double2 su2[36], sxy2[32];
+    su2[threadIdx.x & 31] = make_double2(0.7 + threadIdx.x * 1e-3, 0.3);
+    if ((threadIdx.x & 31) < 4) su2[32 + (threadIdx.x & 31)] = make_double2(0.6, 0.4);
+    __syncwarp();
+    const uint32_t lane = threadIdx.x & 31;
+    double mx = 0, my = 0;
+    for (int i = 0; i < N / 32; ++i) {
+      double2 ring[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) ring[j] = su2[j];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const double2 uj = ring[j % 4];
+        ring[j % 4] = su2[j + 4];
+        x = __dmul_rn(__fma_rn(y, -0.5, 1.0), uj.x);
+        y = __dmul_rn(__fma_rn(x, -0.5, 1.0), uj.y);
+        if (mode == 11) { if (lane == 0) sxy2[j] = make_double2(x, y); }
+        else if (lane == (uint32_t)j) { mx = x; my = y; }
+      }
+    }
+    x += sxy2[lane].x + mx + my;
   } else if (mode == 7) {                  // Gibbs sweep with u from shared memory (LDS.128)
     __shared__ double2 su[64];
     su[threadIdx.x] = make_double2(0.7 + threadIdx.x * 1e-3, 0.3);
@@ -94,8 +116,9 @@ int main(int argc, char** argv) {
   cudaMalloc(&cyc, sizeof(long long));
   const char* names[] = {"DFMA", "DMUL", "DADD", "gibbs sweep (4 fp64)", "SHFL f64 + DADD",
                          "IMAD.WIDE+LOP3", "sweep + 5 stats", "sweep, u from LDS.128",
-                         "sweep + lagged stats", "DFMA x8 indep (per op)", "FFMA x8 indep (per op)"};
-  for (int m = 0; m < 11; ++m) {
+                         "sweep + lagged stats", "DFMA x8 indep (per op)", "FFMA x8 indep (per op)",
+                         "sweep, LDS ring4, STS/step", "sweep, LDS ring4, lane select"};
+  for (int m = 0; m < 13; ++m) {
     if (m == 7 && nthreads > 32) continue;
     long long c = 0;
     for (int rep = 0; rep < 3; ++rep) {
