@@ -229,6 +229,60 @@ __device__ __forceinline__ void sincos2pi_u24(uint32_t w, float* sn, float* cs) 
   *cs = t.x + fmaf(t.x, cm1, -t.y * sb);
   *sn = t.y + fmaf(t.y, cm1, t.x * sb);
 }
+// {sin, cos}(2 pi u53(lo, hi)) for the binary64 Box-Muller angle: k = the
+// 53-bit integer, j = round(k / 2^45) mod 256, rem = k - j 2^45 (|rem| <=
+// 2^44, exact in binary64), b = 2 pi rem 2^-53; table {C_j, S_j} and Taylor
+// sin b to b^7, cos b - 1 to b^6.  ~1e-16 absolute; exact 0/+-1 at the
+// quarter turns, relative-accurate next to the zeros.
+template <class Tab = GlobalTables>
+__device__ __forceinline__ void sincos2pi_u53(uint32_t lo, uint32_t hi, double* sn, double* cs,
+                                              const Tab& tb = Tab()) {
+  const uint64_t k = ((uint64_t)hi << 21) | (lo >> 11);
+  const uint32_t j = (uint32_t)((k + (1ull << 44)) >> 45) & 255u;
+  const int64_t rem = (int64_t)((k - ((uint64_t)j << 45)) << 18) >> 18;
+  const double b = (double)rem * 0x1.921fb54442d18p-51;     // 2 pi / 2^53
+  const double2 t = tb.cs(j);
+  const double b2 = b * b;
+  const double sb = fma(b2 * b, fma(b2, fma(b2, kC[kS7], kC[kS5]), kC[kS3]), b);
+  const double cm1 = b2 * fma(b2, fma(b2, kC[kC6], kC[kC4]), -0.5);
+  *cs = t.x + fma(t.x, cm1, -t.y * sb);
+  *sn = t.y + fma(t.y, cm1, t.x * sb);
+}
+// ln(1 - u53(lo, hi)) (<= 0; exact 0 at u = 0)
+template <class Tab = GlobalTables>
+__device__ __forceinline__ double ln1m_u53(uint32_t lo, uint32_t hi, const Tab& tb = Tab()) {
+  return ln_pos(one_minus_u53(lo, hi), tb);
+}
+// e^y for |y| <= 700 by the table path of exp_nonpos (positive k scales the
+// exponent up, no overflow below 709); libdevice beyond.
+template <class Tab = GlobalTables>
+__device__ __forceinline__ double exp_small(double y, const Tab& tb = Tab()) {
+  if (!(fabs(y) <= 700.0)) return exp(y);
+  const double t = fma(y, kC[kInvLn2x64], kC[kRnd]);
+  const int k = __double2loint(t);
+  const double kd = t - kC[kRnd];
+  double r = fma(kd, -kC[kLn2Hi64], y);
+  r = fma(kd, -kC[kLn2Lo64], r);
+  double q = fma(r, kC[kE6], kC[kE5]);
+  q = fma(r, q, kC[kE4]);
+  q = fma(r, q, kC[kE3]);
+  q = fma(r, q, 0.5);
+  const double p = fma(r * r, q, r);
+  const double T = tb.exp2(k & 63);
+  const double v = fma(T, p, T);
+  return __hiloint2double(__double2hiint(v) + (k >> 6) * (1 << 20), __double2loint(v));
+}
+// Box-Muller pair from one block (R-06, binary64): r = sqrt(-2 ln(1-u53(w0,
+// w1))), theta = 2 pi u53(w2, w3); {r cos, r sin}.
+template <class Tab = GlobalTables>
+__device__ __forceinline__ void box_muller_f64(uint4 w, double* z0, double* z1,
+                                               const Tab& tb = Tab()) {
+  const double r = sqrt_nonneg(-2.0 * ln1m_u53(w.x, w.y, tb));
+  double sn, cs;
+  sincos2pi_u53(w.z, w.w, &sn, &cs, tb);
+  *z0 = r * cs;
+  *z1 = r * sn;
+}
 }  // namespace dm
 
 // ---- Marsaglia-Tsang trial (R-08, R-09) -----------------------------------------
@@ -333,10 +387,9 @@ __device__ __forceinline__ float std_gaussian_f32(const Key& k, uint64_t stream,
 __device__ __forceinline__ double std_gaussian_f64(const Key& k, uint64_t stream, uint64_t base,
                                                    uint64_t i) {
   const uint4 w = block(k, stream, base + i / 2);
-  const double r = sqrt(-2.0 * log(1.0 - u53(w.x, w.y)));
-  double sn, cs;
-  sincospi(2.0 * u53(w.z, w.w), &sn, &cs);
-  return (i % 2) ? r * sn : r * cs;
+  double z0, z1;
+  dm::box_muller_f64(w, &z0, &z1);
+  return (i % 2) ? z1 : z0;
 }
 __device__ __forceinline__ float gaussian_f32(const Key& k, uint64_t stream, uint64_t base,
                                               uint64_t i, float mu, float sigma) {
@@ -354,29 +407,42 @@ __device__ __forceinline__ float exponential_f32(const Key& k, uint64_t stream, 
   const float e = -logf(1.0f - std_uniform_f32(k, stream, base, i));
   return (isfinite(lambda) && lambda > 0.0f) ? e / lambda : nanf_();
 }
+// the word pair of binary64 sample i (two samples per block)
+__device__ __forceinline__ uint2 pair_f64(const Key& k, uint64_t stream, uint64_t base,
+                                          uint64_t i) {
+  const uint4 w = block(k, stream, base + i / 2);
+  return (i % 2) ? make_uint2(w.z, w.w) : make_uint2(w.x, w.y);
+}
 __device__ __forceinline__ double exponential_f64(const Key& k, uint64_t stream, uint64_t base,
                                                   uint64_t i, double lambda) {
-  const double e = -log(1.0 - std_uniform_f64(k, stream, base, i));
+  const uint2 p = pair_f64(k, stream, base, i);
+  const double e = -dm::ln1m_u53(p.x, p.y);
   return (isfinite(lambda) && lambda > 0.0) ? e / lambda : nan_();
 }
 __device__ __forceinline__ double log_uniform_f64(const Key& k, uint64_t stream, uint64_t base,
                                                   uint64_t i) {
-  return log(1.0 - std_uniform_f64(k, stream, base, i));
+  const uint2 p = pair_f64(k, stream, base, i);
+  return dm::ln1m_u53(p.x, p.y);
 }
 // GetLaplace (R-30): mu + beta s e; f32 words (2j, 2j+1) of block i/2, f64 block i
 __device__ __forceinline__ double laplace_f64(const Key& k, uint64_t stream, uint64_t base,
                                               uint64_t i, double mu, double beta) {
   const uint4 w = block(k, stream, base + i);
-  const double e = -log(1.0 - u53(w.x, w.y));
+  const double e = -dm::ln1m_u53(w.x, w.y);
   const double s = u53(w.z, w.w) < 0.5 ? -e : e;
   return (isfinite(mu) && isfinite(beta) && beta > 0.0) ? fma(beta, s, mu) : nan_();
+}
+// e^(ln(e) / alpha) of the Weibull transform (binary64): e = 0 gives 0
+__device__ __forceinline__ double weibull_pow_f64(double e, double alpha) {
+  return dm::exp_small((e > 0.0 ? dm::ln_pos(e) : -INFINITY) / alpha);
 }
 // GetWeibull (R-30): beta e^(1/alpha)
 __device__ __forceinline__ double weibull_f64(const Key& k, uint64_t stream, uint64_t base,
                                               uint64_t i, double alpha, double beta) {
-  const double e = -log(1.0 - std_uniform_f64(k, stream, base, i));
+  const uint2 p = pair_f64(k, stream, base, i);
+  const double e = -dm::ln1m_u53(p.x, p.y);
   return (isfinite(alpha) && isfinite(beta) && alpha > 0.0 && beta > 0.0)
-             ? beta * exp(log(e) / alpha) : nan_();
+             ? beta * weibull_pow_f64(e, alpha) : nan_();
 }
 // GetGamma (R-08..R-11): shape alpha, scale beta; *trial = accepting trial
 // (0 when invalid / capped).  Trials run sequentially here; the bulk kernel

@@ -82,10 +82,13 @@ template <> struct Vec<double, 1> {
 
 __device__ __forceinline__ float fnan() { return __int_as_float(0x7fffffff); }
 __device__ __forceinline__ double dnan() { return __longlong_as_double(0x7ff8000000000000ll); }
-__device__ __forceinline__ float flog(float x) { return logf(x); }
-__device__ __forceinline__ double flog(double x) { return log(x); }
-__device__ __forceinline__ float fexp(float x) { return expf(x); }
-__device__ __forceinline__ double fexp(double x) { return exp(x); }
+// Weibull's e^(ln(e)/alpha): binary32 libm, binary64 the device API's
+__device__ __forceinline__ float weibull_pow(float e, float alpha) {
+  return expf(logf(e) / alpha);
+}
+__device__ __forceinline__ double weibull_pow(double e, double alpha) {
+  return brng_dev::weibull_pow_f64(e, alpha);
+}
 
 // ---- per-sample transforms (validity -> NaN + count, R-23) --------
 template <int DIST, typename T>
@@ -110,7 +113,7 @@ __device__ __forceinline__ T xform(T p0, T p1, T s, uint32_t& bad) {
   } else if (DIST == kWeibull) {          // beta e^(1/alpha)
     const bool ok = isfinite(p0) && isfinite(p1) && (p0 > T(0)) && (p1 > T(0));
     bad += !ok;
-    return ok ? p1 * fexp(flog(s) / p0) : nanv;
+    return ok ? p1 * weibull_pow(s, p0) : nanv;
   }
   return s;
 }
@@ -144,23 +147,23 @@ __device__ __forceinline__ void std_block(uint4 w, float* s) {
 }
 // f64: 2 x u53 (uniform / exponential / log-uniform / Weibull), one Box-Muller
 // pair, or one Laplace sample.
+// (binary64 transcendentals: the table-driven brng_dev::dm functions, the same
+// ones the device-API getters use, so bulk and getter results are identical)
 template <int DIST>
 __device__ __forceinline__ void std_block(uint4 w, double* s) {
+  namespace dm = brng_dev::dm;
   if (DIST == kGaussian) {
-    double sn, cs;
-    const double r = sqrt(-2.0 * log(1.0 - u53(w.x, w.y)));
-    sincospi(2.0 * u53(w.z, w.w), &sn, &cs);
-    s[0] = r * cs; s[1] = r * sn;
+    dm::box_muller_f64(w, &s[0], &s[1]);
   } else if (DIST == kLaplace) {
-    const double e = -log(1.0 - u53(w.x, w.y));
+    const double e = -dm::ln1m_u53(w.x, w.y);
     s[0] = u53(w.z, w.w) < 0.5 ? -e : e;
   } else {
-    const double u[2] = {u53(w.x, w.y), u53(w.z, w.w)};
+    const uint32_t lo[2] = {w.x, w.z}, hi[2] = {w.y, w.w};
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      if (DIST == kExponential || DIST == kWeibull) s[k] = -log(1.0 - u[k]);
-      else if (DIST == kLogUniform) s[k] = log(1.0 - u[k]);
-      else s[k] = u[k];
+      if (DIST == kExponential || DIST == kWeibull) s[k] = -dm::ln1m_u53(lo[k], hi[k]);
+      else if (DIST == kLogUniform) s[k] = dm::ln1m_u53(lo[k], hi[k]);
+      else s[k] = u53(lo[k], hi[k]);
     }
   }
 }

@@ -303,3 +303,50 @@ def test_dm_sincos2pi_u24_accuracy(user_lib):
         big[4:4 + len(near)] = True
         rel = err[big] / np.abs(np.array(ex)[big])
         assert rel.max() <= 4 * 2.0**-24, rel.max()
+
+
+def test_dm_sincos2pi_u53_accuracy(user_lib):
+    """binary64 {sin, cos}(2 pi u53(lo, hi)) (the f64 Box-Muller angle):
+    absolute error <= 2^-53, exact values at the quarter turns, relative
+    accuracy next to the zeros."""
+    import mpmath as mp
+    mp.mp.dps = 40
+    rng = np.random.default_rng(8)
+    ks = [0, 1 << 51, 1 << 52, 3 << 51, (1 << 51) + 1, (1 << 52) - 1, 2**53 - 1, 5, 2**53 - 5,
+          (1 << 44), (1 << 44) - 1, (1 << 45) + (1 << 44)]
+    ks += [int(v) for v in rng.integers(0, 2**53, 4000, dtype=np.int64)]
+    w = []
+    for k in ks:
+        v = k << 11                      # u53 = (hi:lo) >> 11
+        w += [v & 0xFFFFFFFF, v >> 32]
+    sn, cs = _math(user_lib, 8, w=w, n=len(ks)), _math(user_lib, 9, w=w, n=len(ks))
+    ang = [2 * mp.pi * k / mp.mpf(2) ** 53 for k in ks]
+    es, ec = [float(mp.sin(a)) for a in ang], [float(mp.cos(a)) for a in ang]
+    assert list(sn[:4]) == [0.0, 1.0, 0.0, -1.0] and list(cs[:4]) == [1.0, 0.0, -1.0, 0.0]
+    for got, ex in ((sn, es), (cs, ec)):
+        err = np.abs(got - np.array(ex))
+        assert err.max() <= 2.0**-53, err.max()
+    for idx in (4, 5, 6, 7, 8):          # next to zeros of sin or cos
+        for got, ex in ((sn, es), (cs, ec)):
+            if abs(ex[idx]) < 1e-6:
+                assert abs(got[idx] - ex[idx]) <= 2 * abs(ex[idx]) * 2.0**-52
+
+
+def test_dm_exp_small_accuracy(user_lib):
+    """e^y for |y| <= 700 within 2 ulp (both signs: the Weibull transform's
+    ln(e)/alpha), libdevice beyond (overflow to inf, underflow to 0)."""
+    import math
+    import mpmath as mp
+    mp.mp.dps = 40
+    rng = np.random.default_rng(9)
+    y = [0.0, 1.0, -1.0, 700.0, -700.0, 709.0, 710.0, -745.5, 1e-300, -1e-300]
+    y += list(rng.uniform(-700, 700, 3000)) + list(rng.normal(0, 1, 1000))
+    got = _math(user_lib, 10, x=y)
+    for g, v in zip(got, y):
+        e = float(mp.exp(mp.mpf(v))) if v < 709.8 else math.inf
+        if math.isinf(e):
+            assert math.isinf(g)
+        elif e >= 2.0**-1022:
+            assert abs(g - e) <= 2 * math.ulp(e), (v, g, e)
+        else:
+            assert abs(g - e) <= 2 * math.ulp(0.0), (v, g, e)
