@@ -44,8 +44,16 @@ using Tables = brng_dev::dm::GlobalTables;
 // alpha<1 boost work item, parked in a per-warp shared-memory queue so that
 // boosts run as full warps instead of as a divergent branch (36% of cfg3's
 // samples, 91% of cfg4's).
+// 16 bytes: the boost re-reads the sample's alpha, beta (just loaded, so
+// cache hits), which halves the queue's shared memory (occupancy).
+#ifndef BRNG_SLIM_QUEUE
+#define BRNG_SLIM_QUEUE 1
+#endif
 struct BoostItem {
-  double g, alpha, beta;
+  double g;
+#if !BRNG_SLIM_QUEUE
+  double alpha, beta;
+#endif
   uint64_t i_t;            // sample index | trial << 56
 };
 constexpr int kBoostCap = 64;
@@ -81,9 +89,15 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
     if (lane < n) {
       const BoostItem it = q[qn - n + lane];
       const uint64_t ii = it.i_t & 0x00FFFFFFFFFFFFFFull;
+#if BRNG_SLIM_QUEUE
+      double qa, qb;
+      load(ii, qa, qb);
+#else
+      const double qa = it.alpha, qb = it.beta;
+#endif
       const uint4 wb = philox_block_rk(base + (uint64_t)kStride * ii, rk);
-      const double gb = mt_boost(wb, it.g, it.alpha, tb);
-      sink(ii, gb * it.beta, (uint32_t)(it.i_t >> 56));
+      const double gb = mt_boost(wb, it.g, qa, tb);
+      sink(ii, gb * qb, (uint32_t)(it.i_t >> 56));
     }
     qn -= n;
     __syncwarp();
@@ -109,7 +123,10 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
     const uint32_t bm = __ballot_sync(kFull, boost);
     if (boost) {
       BoostItem it;
-      it.g = g; it.alpha = alpha; it.beta = beta;
+      it.g = g;
+#if !BRNG_SLIM_QUEUE
+      it.alpha = alpha; it.beta = beta;
+#endif
       it.i_t = i | ((uint64_t)t << 56);
       q[qn + __popc(bm & lt)] = it;
     }
@@ -173,10 +190,15 @@ struct DirArgs {
   uint64_t n_rows, k, base, stream;
   RoundKeys rk;
   unsigned long long* err;
+  uint32_t rpw;          // rows per warp queue (smem kernel)
 };
 
 constexpr int kDirThreads = 128;     // 4 warps / CTA, one row per warp
 constexpr uint64_t kDirSmemK = 2048; // rows up to this K are staged in smem
+#ifndef BRNG_DIR_TARGET
+#define BRNG_DIR_TARGET 512
+#endif
+constexpr uint64_t kDirTarget = BRNG_DIR_TARGET;   // samples per warp queue (rows grouped)
 
 __device__ __forceinline__ double warp_sum(double s) {
 #pragma unroll
@@ -194,29 +216,38 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __gri
   const Tables tb{};
   BoostItem* q = qs[threadIdx.x >> 5];
   const uint32_t lane = threadIdx.x & 31;
-  double* g_row = gsm + (threadIdx.x >> 5) * a.k;
+  // a.rpw rows per warp queue: one continuous queue over the group's
+  // rpw * k samples, so the lanes idle at a queue's tail once per group
+  // instead of once per row (the rows' values do not depend on the grouping)
+  double* g_grp = gsm + (uint64_t)(threadIdx.x >> 5) * a.rpw * a.k;
   const uint64_t warp = ((uint64_t)blockIdx.x * kDirThreads + threadIdx.x) >> 5;
   const uint64_t n_warps = ((uint64_t)gridDim.x * kDirThreads) >> 5;
+  const uint64_t n_groups = (a.n_rows + a.rpw - 1) / a.rpw;
   uint32_t nbad = 0;
-  for (uint64_t row = warp; row < a.n_rows; row += n_warps) {
-    const uint64_t beg = row * a.k;
+  for (uint64_t grp = warp; grp < n_groups; grp += n_warps) {
+    const uint64_t row0 = grp * a.rpw;
+    const uint64_t rows = a.n_rows - row0 < a.rpw ? a.n_rows - row0 : a.rpw;
+    const uint64_t beg = row0 * a.k;
     mt_queue(
-        beg, beg + a.k, a.base, a.rk, tb,
+        beg, beg + rows * a.k, a.base, a.rk, tb,
         [&](uint64_t i, double& al, double& be) {
           al = (double)__ldg(a.alpha + i);
           be = 1.0;
         },
         [&](uint64_t i, double v, uint32_t t) {
-          g_row[i - beg] = v;
+          g_grp[i - beg] = v;
           if (a.trials) a.trials[i] = (uint8_t)t;
         },
         nbad, q);
     __syncwarp();
-    double s = 0.0;
-    for (uint64_t j = lane; j < a.k; j += 32) s += g_row[j];
-    s = warp_sum(s);
-    const double inv = 1.0 / s;
-    for (uint64_t j = lane; j < a.k; j += 32) a.out[beg + j] = (T)(g_row[j] * inv);
+    for (uint64_t r = 0; r < rows; ++r) {
+      const double* g_row = g_grp + r * a.k;
+      double s = 0.0;
+      for (uint64_t j = lane; j < a.k; j += 32) s += g_row[j];
+      s = warp_sum(s);
+      const double inv = 1.0 / s;
+      for (uint64_t j = lane; j < a.k; j += 32) a.out[beg + r * a.k + j] = (T)(g_row[j] * inv);
+    }
     __syncwarp();
   }
   flush_errors(a.err, nbad);
@@ -270,18 +301,22 @@ template <typename T>
 cudaError_t dirichlet_typed(const T* alpha, uint64_t n_rows, uint64_t k, T* out,
                             uint8_t* trials, uint64_t base, const Ctx& ctx) {
   DirArgs<T> a{alpha, out, trials, n_rows, k, base, ctx.stream_id,
-                 make_round_keys(ctx.k0, ctx.k1, ctx.stream_id), ctx.err};
+                 make_round_keys(ctx.k0, ctx.k1, ctx.stream_id), ctx.err, 1u};
   const uint64_t ctas_needed = (n_rows + 3) / 4;
   if (k <= kDirSmemK) {
-    const size_t smem = (size_t)4 * k * sizeof(double);
+    const uint64_t r = kDirTarget / k;
+    a.rpw = (uint32_t)(r < 1 ? 1 : (r > 8 ? 8 : r));
+    const size_t smem = (size_t)4 * a.rpw * k * sizeof(double);
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(dirichlet_smem_kernel<T>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
       if (e != cudaSuccess) return e;
     }
+    const uint64_t groups = (n_rows + a.rpw - 1) / a.rpw;
+    const uint64_t ctas = (groups + 3) / 4;
     const uint64_t cap = (uint64_t)ctx.num_sms * 16 * 8;
-    const unsigned g = (unsigned)(ctas_needed < cap ? ctas_needed : cap);
+    const unsigned g = (unsigned)(ctas < cap ? ctas : cap);
     dirichlet_smem_kernel<T><<<g, kDirThreads, smem, ctx.stream>>>(a);
   } else {
     const uint64_t cap = (uint64_t)ctx.num_sms * 16 * 8;
