@@ -22,7 +22,15 @@ namespace brng {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr uint64_t kChunk = 1024;          // samples per warp queue (Gamma)
+// Samples per warp queue (Gamma): a queue's tail (lanes idle while its last
+// samples finish) happens once per chunk.  512 / 1024 / 2048 / 4096 samples
+// measured 0.949 / 0.932 / 0.913 / 0.877 ms on cfg3; one chunk per warp of a
+// single resident wave (~14k) 0.974 (no CTAs left to fill the SMs that
+// finish first).
+#ifndef BRNG_GAMMA_CHUNK
+#define BRNG_GAMMA_CHUNK 4096
+#endif
+constexpr uint64_t kChunk = BRNG_GAMMA_CHUNK;
 constexpr uint32_t kStride = 256;          // blocks per sample (R-11)
 constexpr uint32_t kMaxTrial = 255;
 constexpr uint32_t kFull = 0xffffffffu;
@@ -291,7 +299,7 @@ cudaError_t gamma_typed(const T* alpha, const T* beta, T* out, uint8_t* trials, 
                    make_round_keys(ctx.k0, ctx.k1, ctx.stream_id), ctx.err};
   const uint64_t warps_needed = (n + kChunk - 1) / kChunk;
   const uint64_t ctas_needed = (warps_needed + (kThreads / 32) - 1) / (kThreads / 32);
-  const uint64_t cap = (uint64_t)ctx.num_sms * 8;  // one full-occupancy wave
+  const uint64_t cap = (uint64_t)ctx.num_sms * 8;  // two waves of 4 resident CTAs/SM
   const unsigned g = (unsigned)(ctas_needed < cap ? ctas_needed : cap);
   gamma_kernel<T><<<g, kThreads, 0, ctx.stream>>>(a);
   return cudaGetLastError();
