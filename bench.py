@@ -568,7 +568,7 @@ def oracle_sample_rates(budget_s=15.0, threads=None):
 
     def cfg2(kind):
         def make(n):
-            n = max(4, n // 4 * 4)
+            # arrays of exactly n: the slices measure() cuts cover [0, n)
             p2 = {k: v.numpy() for k, v in W.cfg2_params(n, seed=7).items()}
             out = np.empty(n, np.float32)
             f = oracle.lib().orc_gaussian_f32 if kind == "g" else oracle.lib().orc_uniform_f32
