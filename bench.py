@@ -256,7 +256,10 @@ class Workload:
             self.h5, self.c5["n_chains"], self.c5["n_sweeps"], None, None, 0, None, None,
             self.st5, self.fx5, self.tot5))
         if allreduce is not None:
-            allreduce(self.tot5)
+            if ev is not None and "nccl_totals" in ev:
+                run("nccl_totals", lambda: allreduce(self.tot5))
+            else:
+                allreduce(self.tot5)
 
     def destroy(self):
         for h in (self.h1, self.h2, self.h3, self.h4, self.h5):
@@ -293,8 +296,9 @@ def gpu_arm(args):
     torch.cuda.synchronize()
 
     # ---- device-timed region ------------------------------------------------
+    ev_names = list(names) + (["nccl_totals"] if world > 1 else [])
     evs = [{n: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            for n in names} for _ in range(args.steps)]
+            for n in ev_names} for _ in range(args.steps)]
     clocks = Clocks(local)
     if world > 1:
         dist.barrier()
@@ -364,6 +368,13 @@ def gpu_arm(args):
         if ev:
             d["ncu"] = ev
         bd[n] = d
+    if world > 1:     # the one data-path collective (cfg5 totals, 272 doubles)
+        bd["nccl_totals"] = {"ms": round(statistics.mean(
+            e["nccl_totals"][0].elapsed_time(e["nccl_totals"][1]) for e in evs), 4),
+            "what": "all_reduce of the cfg5 totals (272 f64) after the Gibbs kernel",
+            "cfg5_with_nccl_ms": None}
+        bd["nccl_totals"]["cfg5_with_nccl_ms"] = round(per["cfg5_gibbs"] +
+                                                       bd["nccl_totals"]["ms"], 4)
     dom = max(names, key=lambda n: per[n])
     t_dom = per[dom] * 1e-3
     if dom in ("cfg1_gibbs", "cfg5_gibbs"):
