@@ -41,10 +41,12 @@ SMS, SMSP, LANES = 148, 4, 32
 # Gibbs roofline: the sweep is bound by the B200
 # FMA-heavy pipe, which runs every fp64 op (64 lanes/clk/SM) and the 32x32->64
 # IMAD.WIDE of Philox at half that rate (tools/ubench.cu, profiles/).  The
-# algorithmic work of one sweep is 17 wide multiplies (20 Philox products
-# minus the 3 that are constant along a chain) + 9 fp64 ops (2 x (1-y, mul),
-# 5 statistics) = 17*2 + 9 = 43 fp64-pipe slots; peak = 64 x 148 x f_sm.
-GIBBS_PIPE_OPS_PER_SWEEP = 43
+# algorithmic per-chain work of one sweep is 16 wide multiplies (20 Philox
+# products minus the 3 that are constant along a chain and the round-2 M1
+# product, which depends only on the sweep and is computed once per sweep
+# for all chains) + 9 fp64 ops (2 x (1-y, mul), 5 statistics)
+# = 16*2 + 9 = 41 fp64-pipe slots; peak = 64 x 148 x f_sm.
+GIBBS_PIPE_OPS_PER_SWEEP = 41
 FP64_LANES_PER_SM = 64
 # cfg1 (1024 chains) is LATENCY-bound: a chain's sweeps are serial and each
 # sweep's critical path is 4 dependent fp64 ops (fma, mul, fma, mul) at the
@@ -385,7 +387,7 @@ def gpu_arm(args):
                         "sm_max clock; IMAD.WIDE = 2 slots)",
                 "frac": round(achieved * 1e12 / pipe_peak, 4),
                 "algorithmic_per_unit": f"{GIBBS_PIPE_OPS_PER_SWEEP} pipe slots/sweep "
-                                        "(17 IMAD.WIDE x 2 + 9 fp64)",
+                                        "(16 per-chain IMAD.WIDE x 2 + 9 fp64)",
                 "units_per_launch": wl.samples[dom] // 2,
                 "traffic": None}
         tr = ncu_traffic("gibbs_kernel<0, 2, 256>")

@@ -60,6 +60,7 @@ struct GibbsArgs {
   uint32_t n_sweeps, burn_in;   // n_sweeps < 2^23 (host-checked; u32 histogram)
   uint32_t rounds;              // grid-stride rounds (kCPT chains per thread each)
   uint32_t rk0[10], rk1[10];    // Philox round keys k + r*W (kernel constants)
+  uint32_t c3k1_u;              // UHI launches: hi32(stream) ^ k1, the same for every chain
   const double* x0;
   const double* y0;
   double* out_x;
@@ -160,6 +161,22 @@ __device__ __forceinline__ uint4 chain_block(const ChainKey& ck, uint64_t p0, co
   return c;
 }
 
+// UHI (every chain of the launch has the same high stream word): round 2's
+// M1 product depends only on the sweep, so it is computed once per sweep for
+// all chains (uniform datapath) and passed in: 16 per-chain products per
+// sweep instead of 17.
+__device__ __forceinline__ uint4 chain_block_u(const ChainKey& ck, uint64_t p0, uint64_t p1,
+                                               const RoundKeys& rk) {
+  uint4 c;
+  c.x = (uint32_t)(p1 >> 32) ^ ck.d2;
+  c.y = (uint32_t)p1;
+  c.z = (uint32_t)p0 ^ ck.a2;
+  c.w = ck.b2;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) c = philox_round(c, rk.k0[r], rk.k1[r]);
+  return c;
+}
+
 // Per-chain state, scaled: X = x 2^64, Y = y 2^64, S1* = s1 2^64,
 // S2*, SXY = s2 2^128.
 struct Chain {
@@ -169,7 +186,7 @@ struct Chain {
 };
 
 // Sweeps [s_begin, s_end) of the thread's kCPT chains.
-template <bool STORE, bool STATS, int CPT, int UNROLL>
+template <bool STORE, bool STATS, int CPT, int UNROLL, bool UHI>
 __device__ __forceinline__ void sweeps(const GibbsArgs& a, const RoundKeys& rk, uint32_t s_begin,
                                        uint32_t s_end, Chain (&ch)[CPT], uint32_t hist_base) {
   uint32_t s = s_begin;
@@ -185,10 +202,11 @@ __device__ __forceinline__ void sweeps(const GibbsArgs& a, const RoundKeys& rk, 
     uint64_t p0 = (uint64_t)kPhiloxM0 * pos_lo;
 #pragma unroll UNROLL
     for (; s < e; ++s) {
+      const uint64_t p1u = UHI ? (uint64_t)kPhiloxM1 * ((uint32_t)(p0 >> 32) ^ a.c3k1_u) : 0;
 #pragma unroll
       for (int k = 0; k < CPT; ++k) {
         Chain& q = ch[k];
-        const uint4 w = chain_block(ck[k], p0, rk);
+        const uint4 w = UHI ? chain_block_u(ck[k], p0, p1u, rk) : chain_block(ck[k], p0, rk);
         // x = fl(fl(1-y) u53)  <=>  X = fl(fl(1-y) u53 2^64),  1-y = fma(Y, -2^-64, 1)
         q.X = __dmul_rn(__fma_rn(q.Y, -kInvScale, 1.0), u53_scaled(w.x, w.y));
         q.Y = __dmul_rn(__fma_rn(q.X, -kInvScale, 1.0), u53_scaled(w.z, w.w));
@@ -220,7 +238,7 @@ __device__ __forceinline__ double warp_sum(double s) {
 // <.., kCPT, kThreads> (two chains per thread for ILP); small chain counts
 // (cfg1: 1024 chains) use one chain per thread in 64-thread CTAs to spread
 // the latency-bound chains over more SMs.
-template <bool STORE, int CPT, int THREADS>
+template <bool STORE, int CPT, int THREADS, bool UHI>
 __global__ void __launch_bounds__(THREADS, (THREADS == kThreads ? BRNG_GIBBS_MINB : 1))
 gibbs_kernel(GibbsArgs a) {
   constexpr int kW = THREADS / 32;
@@ -261,8 +279,8 @@ gibbs_kernel(GibbsArgs a) {
     // one chain per thread (latency-bound small launches): unroll deeper so
     // the Philox blocks of several sweeps overlap the serial x/y update chain
     constexpr int U = CPT == 1 ? kSmallUnroll : kUnroll;
-    sweeps<STORE, false, CPT, U>(a, rk, 0, a.burn_in, ch, hist_base);
-    sweeps<STORE, true, CPT, U>(a, rk, a.burn_in, a.n_sweeps, ch, hist_base);
+    sweeps<STORE, false, CPT, U, UHI>(a, rk, 0, a.burn_in, ch, hist_base);
+    sweeps<STORE, true, CPT, U, UHI>(a, rk, a.burn_in, a.n_sweeps, ch, hist_base);
 
     double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
@@ -508,11 +526,11 @@ int occupancy(K kernel, int threads) {
   return v;
 }
 int ctas_per_sm_bulk() {
-  static int cached = occupancy(gibbs_kernel<false, kCPT, kThreads>, kThreads);
+  static int cached = occupancy(gibbs_kernel<false, kCPT, kThreads, true>, kThreads);
   return cached;
 }
 int ctas_per_sm_small() {
-  static int cached = occupancy(gibbs_kernel<true, kSmallCPT, kSmallThreads>, kSmallThreads);
+  static int cached = occupancy(gibbs_kernel<true, kSmallCPT, kSmallThreads, false>, kSmallThreads);
   return cached;
 }
 int ctas_per_sm_lat() {
@@ -581,6 +599,14 @@ cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
   a.x0 = x0; a.y0 = y0; a.out_x = out_x; a.out_y = out_y; a.chain_stats = chain_stats;
   a.final_xy = final_xy; a.partials = partials; a.err = ctx.err;
   const bool store = out_x != nullptr || out_y != nullptr;
+  // every chain's stream (stream_id + c) has the same high word?  (the padding
+  // chains of the last round never store or count, so only real ones matter)
+#ifndef BRNG_GIBBS_UHI
+#define BRNG_GIBBS_UHI 1
+#endif
+  const bool uhi = BRNG_GIBBS_UHI &&
+                   (ctx.stream_id >> 32) == ((ctx.stream_id + (n_chains - 1)) >> 32);
+  a.c3k1_u = (uint32_t)(ctx.stream_id >> 32) ^ a.rk1[0];
   unsigned n_parts = grid;
   if (n_chains <= (uint64_t)ctx.num_sms * BRNG_GIBBS_LAT_PER_SM) {
     const uint64_t want = (n_chains + kLatW - 1) / kLatW;
@@ -592,14 +618,19 @@ cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
       gibbs_warp_kernel<false><<<n_parts, kLatThreads, 0, ctx.stream>>>(a);
   } else if (sh.small) {
     if (store)
-      gibbs_kernel<true, kSmallCPT, kSmallThreads><<<grid, kSmallThreads, 0, ctx.stream>>>(a);
+      gibbs_kernel<true, kSmallCPT, kSmallThreads, false><<<grid, kSmallThreads, 0, ctx.stream>>>(a);
     else
-      gibbs_kernel<false, kSmallCPT, kSmallThreads><<<grid, kSmallThreads, 0, ctx.stream>>>(a);
+      gibbs_kernel<false, kSmallCPT, kSmallThreads, false><<<grid, kSmallThreads, 0, ctx.stream>>>(a);
+  } else if (uhi) {
+    if (store)
+      gibbs_kernel<true, kCPT, kThreads, true><<<grid, kThreads, 0, ctx.stream>>>(a);
+    else
+      gibbs_kernel<false, kCPT, kThreads, true><<<grid, kThreads, 0, ctx.stream>>>(a);
   } else {
     if (store)
-      gibbs_kernel<true, kCPT, kThreads><<<grid, kThreads, 0, ctx.stream>>>(a);
+      gibbs_kernel<true, kCPT, kThreads, false><<<grid, kThreads, 0, ctx.stream>>>(a);
     else
-      gibbs_kernel<false, kCPT, kThreads><<<grid, kThreads, 0, ctx.stream>>>(a);
+      gibbs_kernel<false, kCPT, kThreads, false><<<grid, kThreads, 0, ctx.stream>>>(a);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || totals == nullptr) return e;

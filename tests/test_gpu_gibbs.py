@@ -179,3 +179,18 @@ def test_launch_shapes_agree_across_the_latency_threshold():
     # histogram of the first thr chains is the same whichever kernel counted it
     extra = _run(42, 5 + thr, 1000, 37, ns, burn)
     assert np.array_equal(lo["totals"][HDR:] + extra["totals"][HDR:], hi["totals"][HDR:])
+
+
+@pytest.mark.parametrize("stream_id", [0, (1 << 32) - 40_000, (5 << 32) + 123])
+def test_bulk_launch_high_stream_word(stream_id):
+    """The bulk launch computes round 2's M1 product once per sweep when every
+    chain's stream has the same high word, per chain otherwise (a launch whose
+    streams cross a 2^32 boundary).  Both must give the oracle's chains:
+    sampled chains on both sides of the boundary, bit-exact."""
+    n_chains, ns = 80_000, 12                      # above half a bulk wave
+    g = _run(77, stream_id, 5, n_chains, ns, samples=True)
+    for c in (0, 1, 39_999, 40_000, 40_001, n_chains - 1):
+        r = oracle.gibbs_triangle(77, stream_id + c, 5, 1, ns)
+        assert np.array_equal(g["out_x"][:, c], r["out_x"][:, 0]), c
+        assert np.array_equal(g["out_y"][:, c], r["out_y"][:, 0]), c
+        assert np.array_equal(g["chain_stats"][:, c], r["chain_stats"][:, 0]), c
