@@ -35,7 +35,7 @@ namespace {
 
 constexpr int kThreads = 256;
 #ifndef BRNG_GIBBS_CPT
-#define BRNG_GIBBS_CPT 2
+#define BRNG_GIBBS_CPT 3
 #endif
 #ifndef BRNG_GIBBS_MINB
 #define BRNG_GIBBS_MINB 2
