@@ -87,7 +87,7 @@ def ncu_traffic(kernel_substr):
 NCU_KERNEL = {"cfg1_gibbs": "gibbs_warp_kernel<1>", "cfg2_gaussian": "fill_kernel<float, 3, 0>",
               "cfg2_uniform": "fill_kernel<float, 2, 0>", "cfg3_gamma": "gamma_kernel<double>",
               "cfg4_dirichlet": "dirichlet_smem_kernel<float>",
-              "cfg5_gibbs": "gibbs_kernel<0, 2, 256>"}
+              "cfg5_gibbs": "gibbs_kernel<0, 3, 256, 1>"}
 
 
 def ncu_evidence(kernel_substr):
@@ -390,7 +390,7 @@ def gpu_arm(args):
                                         "(16 per-chain IMAD.WIDE x 2 + 9 fp64)",
                 "units_per_launch": wl.samples[dom] // 2,
                 "traffic": None}
-        tr = ncu_traffic("gibbs_kernel<0, 2, 256>")
+        tr = ncu_traffic(NCU_KERNEL["cfg5_gibbs"])
         if tr is not None:
             roof["traffic"] = int(tr[0])
             roof["traffic_source"] = tr[1] + " (ncu --set full, dram__bytes_read+write per "\
