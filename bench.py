@@ -389,15 +389,18 @@ def gpu_arm(args):
                 "algorithmic_per_unit": f"{GIBBS_PIPE_OPS_PER_SWEEP} pipe slots/sweep "
                                         "(16 per-chain IMAD.WIDE x 2 + 9 fp64)",
                 "units_per_launch": wl.samples[dom] // 2,
-                "traffic": None}
+                "traffic": None,
+                "peak_source": "derived (DESIGN.md §7): 64 fp64 lanes/clk/SM (tools/ubench.cu "
+                               "measures 62 DFMA/clk/SM) x 148 SMs x the sampled sm_max clock"}
         tr = ncu_traffic(NCU_KERNEL["cfg5_gibbs"])
         if tr is not None:
             roof["traffic"] = int(tr[0])
             roof["traffic_source"] = tr[1] + " (ncu --set full, dram__bytes_read+write per "\
                 "launch; algorithmic = chain_stats + final_xy writes 0.94 GB)"
     else:
-        roof = {"kernel": dom, "bound": bd[dom].get("bound"), "frac": bd[dom].get("frac")}
-    roof["peak_source"] = peak_kind
+        roof = {"kernel": dom, "bound": bd[dom].get("bound"), "frac": bd[dom].get("frac"),
+                "peak_source": peak_kind}
+    roof["hbm_peak_source"] = f"{peak_kind} ({hbm_peak:.1f} GB/s, MEASURED_PEAKS.json; fills)"
 
     # ---- end to end through the C ABI with host buffers ----------------------
     e2e = None
