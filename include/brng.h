@@ -47,8 +47,13 @@
  *            BRNG_ERR_CUDA (cursor unchanged).
  *  Precision. f32 entry points read/write binary32 and compute the reducible
  *            transforms in binary32; Gamma/Dirichlet compute in binary64
- *            internally for every output type (R-28); Gibbs is binary64.
- *            No fast-math: IEEE division/sqrt, denormals preserved.
+ *            internally for every output type (R-28); Gibbs is binary64
+ *            with IEEE sub/mul/fma only (bit-exact).  No fast-math; denormals
+ *            preserved.  Transcendentals: binary32 libm (logf, sqrtf) plus a
+ *            table sincos for the f32 fills; binary64 fills and the Gamma
+ *            trial/boost use the library's table-driven ln/cos/exp and a
+ *            Newton rsqrt (1-2 ulp, include/brng_device.cuh),
+ *            well inside the 2e-6 / 1e-12 parity tolerances.
  */
 #ifndef BRNG_H
 #define BRNG_H
