@@ -412,17 +412,7 @@ def gpu_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "one step = BASELINE.json configs[0..4] at full size per GPU "
-                               "(cfg1 Gibbs 1024x1000 + cfg2 Gaussian&uniform 2^28 f32 + cfg3 "
-                               "Gamma 2^26 f64 + cfg4 Dirichlet 1e6x256 f32 + cfg5 Gibbs "
-                               "2^24x4096)" + (" [--small: NOT a bench number]" if args.small
-                                               else ""),
-                   "sample_unit": "one output deviate (Gibbs: one conditional draw)",
-                   "samples_per_gpu_step": sum(wl.samples.values()),
-                   "l2": "inputs larger than L2 (each step streams ~9 GB of parameters/outputs)",
-                   "dtypes": {"cfg1": "f64", "cfg2": "f32", "cfg3": "f64", "cfg4": "f32 io, f64 "
-                              "internal", "cfg5": "f64"},
-                   "parallelism": f"dp{world} (disjoint Philox counter ranges)"},
+        "config": step_config(world, args.small),
         "roofline": roof,
         "breakdown": bd,
         "gpu_launches": wl.launches_per_step * args.steps,
@@ -645,6 +635,20 @@ def cpu_baseline(budget_s):
             "per_config_Msamples_per_s": {k: round(v / 1e6, 3) for k, v in rates.items()}}
 
 
+def step_config(world, small=False):
+    """The `config` object of a bench line (both arms): the workload of one step."""
+    return {"workload": "one step = BASELINE.json configs[0..4] at full size per GPU "
+                        "(cfg1 Gibbs 1024x1000 + cfg2 Gaussian&uniform 2^28 f32 + cfg3 "
+                        "Gamma 2^26 f64 + cfg4 Dirichlet 1e6x256 f32 + cfg5 Gibbs "
+                        "2^24x4096)" + (" [--small: NOT a bench number]" if small else ""),
+            "sample_unit": "one output deviate (Gibbs: one conditional draw)",
+            "samples_per_gpu_step": sum(step_samples().values()),
+            "l2": "inputs larger than L2 (each step streams ~9 GB of parameters/outputs)",
+            "dtypes": {"cfg1": "f64", "cfg2": "f32", "cfg3": "f64",
+                       "cfg4": "f32 io, f64 internal", "cfg5": "f64"},
+            "parallelism": f"dp{world} (disjoint Philox counter ranges)"}
+
+
 def reference_arm(args):
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
@@ -665,8 +669,7 @@ def reference_arm(args):
            "warmup": args.warmup, "ms_per_step": round(sum(s.values()) / (v * 1e9) * 1e3, 3),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "impl": "reference",
-           "config": {"workload": "same step as the GPU arm, timed as bounded samples and "
-                                  "projected (see cpu_baseline.sample)"},
+           "config": step_config(int(os.environ.get("WORLD_SIZE", 1))),
            "cpu_baseline": {"value": round(v, 6), "unit": UNIT, "cores": P, "kind": "oracle",
                             "sample": desc},
            "e2e": {"value": round(v, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
