@@ -263,6 +263,22 @@ class Workload:
             else:
                 allreduce(self.tot5)
 
+    def checksums(self):
+        """Bit-level checksums of every output of a step (sum of the raw 32-bit
+        words, exact), to show the step is deterministic across repetitions."""
+        torch = self.torch
+        outs = {"cfg1_gibbs": (self.o1x, self.o1y, self.tot1), "cfg2_gaussian": (self.o2g,),
+                "cfg2_uniform": (self.o2u,), "cfg3_gamma": (self.o3,),
+                "cfg4_dirichlet": (self.o4,), "cfg5_gibbs": (self.st5, self.fx5, self.tot5)}
+        res = {}
+        for name, ts in outs.items():
+            h = 0
+            for t in ts:
+                h = (h * 1000003 + int(t.contiguous().view(torch.int32).to(torch.int64).sum()
+                                       .item())) % (1 << 61)
+            res[name] = h
+        return res
+
     def destroy(self):
         for h in (self.h1, self.h2, self.h3, self.h4, self.h5):
             self.B.brng_destroy(h)
@@ -323,6 +339,15 @@ def gpu_arm(args):
         ms = tt.item()
     ms_step = ms / args.steps
     per = {n: statistics.mean(e[n][0].elapsed_time(e[n][1]) for e in evs) for n in names}
+    # determinism: the outputs of the last timed step vs one more (untimed) step
+    # (cfg5 totals include the all-reduce, so they are compared at N = 1 only)
+    cs_a = wl.checksums()
+    wl.step(allreduce=allreduce)
+    torch.cuda.synchronize()
+    cs_b = wl.checksums()
+    determinism = {"identical_across_steps": all(cs_a[k] == cs_b[k] for k in cs_a
+                                                 if world == 1 or k != "cfg5_gibbs"),
+                   "checksums": {k: f"{v:016x}" for k, v in cs_a.items()}}
     total_samples = sum(wl.samples.values()) * world
     value = total_samples / (ms_step * 1e-3) / 1e9
     errs = sum(B.brng_device_errors(h) for h in (wl.h1, wl.h2, wl.h3, wl.h4, wl.h5))
@@ -415,6 +440,7 @@ def gpu_arm(args):
         "config": step_config(world, args.small),
         "roofline": roof,
         "breakdown": bd,
+        "determinism": determinism,
         "gpu_launches": wl.launches_per_step * args.steps,
         "device_errors": errs,
         "clocks": clk,
