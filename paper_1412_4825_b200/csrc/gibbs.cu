@@ -12,7 +12,9 @@
 // Philox (4 cycles/warp) and every fp64 op (2 cycles/warp).  So:
 //   * the parts of Philox that are constant along a chain are hoisted
 //     (17 IMAD.WIDE per block instead of 20; the round-1 product is advanced
-//     with a 64-bit add);
+//     with a 64-bit add), and when all chains of a launch share the high
+//     stream word, round 2's M1 product is computed once per sweep for all of
+//     them (uniform datapath): 16 per-chain products;
 //   * the chain state is kept SCALED by 2^64: X = x 2^64 = fl(fl(1-y) u53 2^64)
 //     where u53 2^64 is the Philox word pair with its low 11 bits cleared,
 //     converted exactly by one I2F.F64.U64 (XU pipe), and 1-x =
@@ -22,7 +24,7 @@
 //     arithmetic while saving the two u53 scalings and their shifts;
 //   * the histogram bin floor(256 x) = floor(X 2^-56) is read from the bits
 //     of X with integer ops (ALU pipe), not fp64;
-//   * each thread runs two chains interleaved (ILP) with the round keys in
+//   * each thread runs three chains interleaved (ILP) with the round keys in
 //     the kernel-parameter constant bank.
 // Only IEEE sub/mul/fma are used, with explicit _rn intrinsics so nvcc cannot
 // contract them: samples, final states, per-chain statistics and histogram are
@@ -235,7 +237,7 @@ __device__ __forceinline__ double warp_sum(double s) {
 }
 
 // THREADS threads x CPT chains per thread.  The bulk configuration is
-// <.., kCPT, kThreads> (two chains per thread for ILP); small chain counts
+// <.., kCPT, kThreads> (kCPT = 3 chains per thread for ILP); small chain counts
 // (cfg1: 1024 chains) use one chain per thread in 64-thread CTAs to spread
 // the latency-bound chains over more SMs.
 template <bool STORE, int CPT, int THREADS, bool UHI>
