@@ -324,9 +324,12 @@ def gpu_arm(args):
     clocks.start()
     time.sleep(0.3)
     t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     t0.record()
+    marks[0].record()
     for k in range(args.steps):
         wl.step(ev=evs[k], allreduce=allreduce)
+        marks[k + 1].record()
     t1.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -338,6 +341,7 @@ def gpu_arm(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = tt.item()
     ms_step = ms / args.steps
+    step_ms = [marks[k].elapsed_time(marks[k + 1]) for k in range(args.steps)]
     per = {n: statistics.mean(e[n][0].elapsed_time(e[n][1]) for e in evs) for n in names}
     # determinism: the outputs of the last timed step vs one more (untimed) step
     # (cfg5 totals include the all-reduce, so they are compared at N = 1 only)
@@ -440,6 +444,10 @@ def gpu_arm(args):
         "config": step_config(world, args.small),
         "roofline": roof,
         "breakdown": bd,
+        "step_ms": {"median": round(statistics.median(step_ms), 3),
+                    "best": round(min(step_ms), 3), "worst": round(max(step_ms), 3),
+                    "note": "this rank's per-step device times; value uses the mean over "
+                            "all steps, max over ranks"},
         "determinism": determinism,
         "gpu_launches": wl.launches_per_step * args.steps,
         "device_errors": errs,
