@@ -187,6 +187,27 @@ def test_cfg2_full_size_sampled():
     assert_ks_uniform(pit_uniform(x, a, b), "cfg2 uniform PIT")
 
 
+def test_exponential_full_size_sampled():
+    """SURVEY.md §8(d) extra on-path check: exponential f32 at N = 2^28,
+    lambda ~ logU(1e-3, 1e3) (seed 7), deviates on stream 5."""
+    n = 1 << 28
+    lam = workloads.exp_params(n, seed=7, device=dev())
+    out = torch.empty(n, device=dev())
+    with handle(7, 5) as h:
+        B.brng_exponential_f32(h, lam, out, n)
+        assert B.brng_device_errors(h) == 0
+        assert B.brng_get_offset(h) == n // 4
+    for lo, hi in parity.windows(n, 48, 512, seed=3):
+        ref, sc = parity.fill_reference("exponential", 7, 5, 0, [lam[lo:hi].cpu().numpy()],
+                                        lo, np.float32)
+        parity.check_close(out[lo:hi], ref, sc, np.float32, f"exp 2^28 [{lo},{hi})")
+    from tests.stats_util import assert_ks_uniform, pit_exponential
+    idx = torch.arange(0, n, n >> 20, device=dev())
+    x = out[idx].double().cpu().numpy()
+    assert np.all(x >= 0) and np.all(np.isfinite(x))
+    assert_ks_uniform(pit_exponential(x, lam[idx].double().cpu().numpy()), "exp 2^28 PIT")
+
+
 def test_host_pipeline_multi_chunk_equals_device():
     # > 64 MB per array: the host path runs as several pipelined chunks
     n = 40_000_003
