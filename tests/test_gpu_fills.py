@@ -187,6 +187,7 @@ def test_cfg2_full_size_sampled():
     assert_ks_uniform(pit_uniform(x, a, b), "cfg2 uniform PIT")
 
 
+@pytest.mark.slow
 def test_exponential_full_size_sampled():
     """SURVEY.md §8(d) extra on-path check: exponential f32 at N = 2^28,
     lambda ~ logU(1e-3, 1e3) (seed 7), deviates on stream 5."""
@@ -312,3 +313,23 @@ def test_batch_fill_equals_constant_arrays():
     with handle(1) as h:
         with pytest.raises(B.brng.BrngError):
             B.brng_batch_fill(h, 5, 0, 0.0, 1.0, torch.empty(4, device=dev()), 4)
+
+
+@pytest.mark.slow
+def test_fill_beyond_2_31_samples():
+    """64-bit indexing: n = 2^31 + 7 f32 uniforms (8.6 GB per array); sampled
+    windows and the ragged tail match the oracle."""
+    n = (1 << 31) + 7
+    a = torch.zeros(n, device=dev())
+    b = torch.full((n,), 2.0, device=dev())
+    out = torch.empty(n, device=dev())
+    with handle(21, 4, 3) as h:
+        B.brng_uniform_f32(h, a, b, out, n)
+        assert B.brng_get_offset(h) == 3 + (n + 3) // 4
+    for lo, hi in list(parity.windows(n, 16, 256, seed=5)) + [(n - 9, n)]:
+        ref, sc = parity.fill_reference("uniform", 21, 4, 3, [a[lo:hi].cpu().numpy(),
+                                                               b[lo:hi].cpu().numpy()],
+                                        lo, np.float32)
+        parity.check_close(out[lo:hi], ref, sc, np.float32, f"2^31+ [{lo},{hi})")
+    del a, b, out
+    torch.cuda.empty_cache()

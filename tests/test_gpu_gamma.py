@@ -204,3 +204,29 @@ def test_host_pipeline_multi_chunk_gamma_dirichlet():
         xd = torch.empty(D, K, device=dev())
         B.brng_dirichlet_f32(h, al.to(dev()), D, K, xd, None)
     assert np.array_equal(xh, xd.cpu().numpy())
+
+
+@pytest.mark.slow
+def test_dirichlet_beyond_2_31_components():
+    """64-bit indexing: D*K = 2^31 + 129 components (f32, 8.6 GB each way);
+    sampled rows, including the last one, match the oracle."""
+    K = 129
+    D = (1 << 31) // K + 2
+    assert D * K > (1 << 31)
+    alpha = torch.full((D, K), 0.5, dtype=torch.float32, device=dev())
+    out = torch.empty(D, K, device=dev())
+    tr = torch.empty(D, K, dtype=torch.uint8, device=dev())
+    with handle(5, 3, 11) as h:
+        B.brng_dirichlet_f32(h, alpha, D, K, out, tr)
+        assert B.brng_device_errors(h) == 0
+        assert B.brng_get_offset(h) == 11 + 256 * D * K
+    tot = dict(n=0, n_tie=0, n_fail=0)
+    wins = list(parity.windows(D, 6, 4, seed=9)) + [(D - 4, D)]
+    for lo, hi in wins:
+        r = parity.dirichlet_compare(out[lo:hi], tr[lo:hi], alpha[lo:hi].cpu().numpy(), 5, 3, 11,
+                                     row0=lo, dtype=np.float32)
+        for k in tot:
+            tot[k] += r[k]
+    _assert_decisions(tot, "dirichlet > 2^31")
+    del alpha, out, tr
+    torch.cuda.empty_cache()
