@@ -84,7 +84,7 @@ def ncu_traffic(kernel_substr):
     return best
 
 
-NCU_KERNEL = {"cfg1_gibbs": "gibbs_warp_kernel<1>", "cfg2_gaussian": "fill_kernel<float, 3, 0>",
+NCU_KERNEL = {"cfg1_gibbs": "gibbs_lat_kernel<1>", "cfg2_gaussian": "fill_kernel<float, 3, 0>",
               "cfg2_uniform": "fill_kernel<float, 2, 0>", "cfg3_gamma": "gamma_kernel<double>",
               "cfg4_dirichlet": "dirichlet_smem_kernel<float>",
               "cfg5_gibbs": "gibbs_kernel<0, 3, 256, 1>"}

@@ -371,18 +371,44 @@ __global__ void __launch_bounds__(kRedThreads) reduce_partials_kernel(const doub
 constexpr int kSmallThreads = 64;
 constexpr int kSmallCPT = 1;
 
-// ---- latency mode: one WARP per chain (small chain counts, e.g. cfg1) ------------
+// ---- latency mode (small chain counts, e.g. cfg1) -------------------------
 // With few chains a thread-per-chain launch leaves the GPU nearly empty and
-// each thread walks its 1000+ sweeps serially (Philox + update per sweep).
-// Here the 32 lanes of a warp compute the Philox blocks of 32 consecutive
-// sweeps of ONE chain in parallel (the blocks do not depend on the state),
-// then every lane runs the serial update x = (1-y) u, y = (1-x) u' over those
-// 32 sweeps with the uniforms broadcast by shuffles (same arithmetic, same
-// order: bit-identical samples and statistics).  Lane j keeps sweep j's
-// (x, y) for the histogram and the stores.  The critical path is the 4
-// dependent fp64 ops of a sweep; everything else is off it.
-constexpr int kLatThreads = 128;                 // 4 warps = 4 chains per CTA
-constexpr int kLatW = kLatThreads / 32;
+// each thread walks its 1000+ sweeps serially.  Here the sweep loop of a chain
+// runs with nothing else in its instruction stream:
+//  * a CHAIN warp runs kCPW = 4 chains (8 lanes each, redundantly computing
+//    the same chain): the dependent update x = (1-y) u, y = (1-x) u' and the
+//    five running statistics, 32 sweeps per batch, the uniforms read from a
+//    shared row 4 sweeps ahead of use; the first lane of each chain records
+//    every sweep's state in a shared row.  Several chains per warp share one
+//    instruction stream, so cfg1's 1024 chains need 256 chain warps, fewer
+//    than the 592 SM sub-partitions.
+//  * its HELPER warp computes the Philox blocks of the next batch (one sweep
+//    per lane, every chain of the warp) and, for the previous batch, the
+//    histogram and the sample stores.
+// The pair meets at one named barrier per batch (double-buffered rows).
+// Warp w runs on sub-partition w % 4: chain warps 0, 1 and helpers 2, 3 never
+// share one, so Philox's IMAD.WIDEs stay off the chain's FMA-heavy pipe.
+// Measured (tools/lat_probe.py, tools/ulat2.cu): the one-warp-
+// per-chain kernel with Philox in the chain's own stream took 44 us for cfg1;
+// this one ~21 us, the chain itself ~42 cycles/sweep against the 32-cycle
+// dependency floor.  Same operations in the same order as the oracle:
+// bit-identical samples and statistics (tests compare all launch shapes
+// chain by chain).
+#ifndef BRNG_LAT_RING
+#define BRNG_LAT_RING 4
+#endif
+#ifndef BRNG_LAT_PAIRS
+#define BRNG_LAT_PAIRS 2
+#endif
+#ifndef BRNG_LAT_CPW
+#define BRNG_LAT_CPW 4
+#endif
+constexpr int kRing = BRNG_LAT_RING;             // uniform lookahead (sweeps)
+constexpr int kPairs = BRNG_LAT_PAIRS;           // chain warps per CTA
+constexpr int kCPW = BRNG_LAT_CPW;               // chains per chain warp
+constexpr int kLPC = 32 / kCPW;                  // lanes per chain
+constexpr int kLatThreads = 2 * kPairs * 32;     // + one helper warp each
+constexpr int kLatChains = kCPW * kPairs;        // chains per CTA per round
 
 // All 10 rounds (no per-chain hoisting: 32 sweeps per lane-block here).
 __device__ __forceinline__ uint4 gibbs_block(uint64_t pos, uint64_t stream, const GibbsArgs& a) {
@@ -393,125 +419,176 @@ __device__ __forceinline__ uint4 gibbs_block(uint64_t pos, uint64_t stream, cons
   return c;
 }
 
+__device__ __forceinline__ void pair_bar(uint32_t p) {
+  asm volatile("bar.sync %0, 64;" ::"r"(p + 1) : "memory");
+}
+
 struct WarpChain {
   double X, Y, S1X, S2X, S1Y, S2Y, SXY;
 };
 
-// Serial update of sweeps s0 .. s0+n-1 (n = 32 unrolled when FULL).  The
-// uniforms of sweep j come from the warp's shared row u[j] (one broadcast
-// LDS.128 per sweep, issued ahead of the dependent chain); lane 0 records
-// sweep j's scaled (X, Y) in xy[j].  STATS: 1 all sweeps, 2 sweeps >= burn_in.
-// (Only the full, all-statistics batch is unrolled: the other cases are rare
-// and a second unrolled copy doubles the loop's instruction footprint.)
+// Serial update of one batch: sweeps s0 .. s0+nb-1 with uniforms u[j]; the
+// recording lane stores sweep j's scaled (X, Y) in xy[j].  STATS: 1 all
+// sweeps, 2 sweeps >= burn_in.  A full batch reads its uniforms kRing sweeps
+// ahead through a register ring (ptxas then keeps the loads off the chain's
+// path: 37 vs 54 cycles/sweep for all 32 loaded up front, tools/ulat2.cu).
+// (Only the full, all-statistics batch is unrolled.)
 template <int STATS, bool FULL>
-__device__ __forceinline__ void warp_steps(WarpChain& q, const double2* u, double2* xy,
-                                           bool lane0, uint32_t nb, uint32_t s0,
-                                           uint32_t burn_in) {
-  const int n = FULL ? 32 : (int)nb;
-  double2 un = u[0];                  // one sweep of lookahead on the LDS
-#pragma unroll (FULL ? 32 : 1)
-  for (int j = 0; j < n; ++j) {
-    const double2 uj = un;
-    if (j + 1 < n) un = u[j + 1];
-    q.X = __dmul_rn(__fma_rn(q.Y, -kInvScale, 1.0), uj.x);
-    q.Y = __dmul_rn(__fma_rn(q.X, -kInvScale, 1.0), uj.y);
-    if (STATS == 1 || (STATS == 2 && s0 + (uint32_t)j >= burn_in)) {
+__device__ __forceinline__ void warp_batch(WarpChain& q, const double2* u, double2* xy, bool rec,
+                                           uint32_t nb, uint32_t s0, uint32_t burn_in) {
+  if (FULL) {
+    double2 ring[kRing];
+#pragma unroll
+    for (int j = 0; j < kRing; ++j) ring[j] = u[j];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double2 uj = ring[j % kRing];
+      if (j + kRing < 32) ring[j % kRing] = u[j + kRing];
+      q.X = __dmul_rn(__fma_rn(q.Y, -kInvScale, 1.0), uj.x);
+      q.Y = __dmul_rn(__fma_rn(q.X, -kInvScale, 1.0), uj.y);
       q.S1X = __dadd_rn(q.S1X, q.X); q.S2X = __fma_rn(q.X, q.X, q.S2X);
       q.S1Y = __dadd_rn(q.S1Y, q.Y); q.S2Y = __fma_rn(q.Y, q.Y, q.S2Y);
       q.SXY = __fma_rn(q.X, q.Y, q.SXY);
+      if (rec) xy[j] = make_double2(q.X, q.Y);
     }
-    if (lane0) xy[j] = make_double2(q.X, q.Y);
+  } else {
+    for (int j = 0; j < (int)nb; ++j) {
+      const double2 uj = u[j];
+      q.X = __dmul_rn(__fma_rn(q.Y, -kInvScale, 1.0), uj.x);
+      q.Y = __dmul_rn(__fma_rn(q.X, -kInvScale, 1.0), uj.y);
+      if (STATS == 1 || s0 + (uint32_t)j >= burn_in) {
+        q.S1X = __dadd_rn(q.S1X, q.X); q.S2X = __fma_rn(q.X, q.X, q.S2X);
+        q.S1Y = __dadd_rn(q.S1Y, q.Y); q.S2Y = __fma_rn(q.Y, q.Y, q.S2Y);
+        q.SXY = __fma_rn(q.X, q.Y, q.SXY);
+      }
+      if (rec) xy[j] = make_double2(q.X, q.Y);
+    }
   }
 }
 
 template <bool STORE>
-__global__ void __launch_bounds__(kLatThreads) gibbs_warp_kernel(GibbsArgs a) {
+__global__ void __launch_bounds__(kLatThreads) gibbs_lat_kernel(GibbsArgs a) {
   __shared__ __align__(1024) uint32_t hist[512];   // [256..511]: sink for dead chains
-  __shared__ double red[kLatW][8];
-  __shared__ double2 su[kLatW][32], sxy[kLatW][32];   // per warp: uniforms, states
+  __shared__ double red[kLatChains][8];
+  __shared__ double2 su[kPairs][2][kCPW][32];     // [pair][buffer][chain][sweep] uniforms
+  __shared__ double2 sxy[kPairs][2][kCPW][32];    // [pair][buffer][chain][sweep] states
   const uint32_t hist_base = (uint32_t)__cvta_generic_to_shared(hist);
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double2* const u = su[wid];
-  double2* const xy = sxy[wid];
-  const bool lane0 = lane == 0;
+  // chain warps first: warp w runs on sub-partition w % 4, so with two pairs
+  // the chain warps (0, 1) and their helpers (2, 3) never share one
+  const bool helper = wid >= (uint32_t)kPairs;
+  const uint32_t p = helper ? wid - kPairs : wid;
   for (int b = threadIdx.x; b < 512; b += kLatThreads) hist[b] = 0;
-  if (lane < 8) red[wid][lane] = 0.0;
+  if (threadIdx.x < kLatChains * 8) red[threadIdx.x >> 3][threadIdx.x & 7] = 0.0;
   uint32_t nbad = 0;
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-  const double n = (double)(a.n_sweeps - a.burn_in);
-  const double nm1 = __dsub_rn(n, 1.0);
   __syncthreads();
-  const uint64_t stride = (uint64_t)gridDim.x * kLatW;
-  for (uint64_t c = (uint64_t)blockIdx.x * kLatW + wid; c < a.n_chains; c += stride) {
-    const double x0 = a.x0 ? a.x0[c] : 0.5;
-    const double y0 = a.y0 ? a.y0[c] : 0.5;
-    const bool live = (y0 >= 0.0) && (y0 <= 1.0);
-    nbad += (lane == 0 && !live);
-    WarpChain q;
-    q.X = __dmul_rn(x0, kScale);
-    q.Y = __dmul_rn(live ? y0 : qnan, kScale);
-    q.S1X = q.S2X = q.S1Y = q.S2Y = q.SXY = 0.0;
-    const uint64_t stream = a.stream_id + c;
-    const uint32_t hb = live ? hist_base : hist_base + 1024u;
-    // the Philox blocks of batch b+1 are computed while batch b's serial
-    // updates run (independent work the scheduler interleaves)
-    uint4 w = gibbs_block(a.base + lane, stream, a);
-    for (uint32_t s0 = 0; s0 < a.n_sweeps; s0 += 32) {
-      const uint32_t nb = a.n_sweeps - s0 < 32u ? a.n_sweeps - s0 : 32u;
-      __syncwarp();
-      u[lane] = make_double2(u53_scaled(w.x, w.y), u53_scaled(w.z, w.w));
-      __syncwarp();
-      if (s0 + 32 < a.n_sweeps) w = gibbs_block(a.base + s0 + 32 + lane, stream, a);
-      if (nb == 32 && s0 >= a.burn_in)
-        warp_steps<1, true>(q, u, xy, lane0, nb, s0, a.burn_in);
-      else
-        warp_steps<2, false>(q, u, xy, lane0, nb, s0, a.burn_in);
-      __syncwarp();
-      if (lane < nb) {
-        const double2 st = xy[lane];
-        const double myX = st.x, myY = st.y;
+  const uint64_t n_pairs = (a.n_chains + kCPW - 1) / kCPW;   // chain groups
+  const uint64_t stride = (uint64_t)gridDim.x * kPairs;
+  for (uint64_t cp = (uint64_t)blockIdx.x * kPairs + p; cp < n_pairs; cp += stride) {
+    const uint64_t c0 = (uint64_t)kCPW * cp;
+    if (helper) {
+      bool ex[kCPW], lv[kCPW];
+      uint32_t hb[kCPW];
+#pragma unroll
+      for (int h = 0; h < kCPW; ++h) {
+        ex[h] = c0 + h < a.n_chains;
+        const double y0 = (ex[h] && a.y0) ? a.y0[c0 + h] : 0.5;
+        lv[h] = ex[h] && (y0 >= 0.0) && (y0 <= 1.0);
+        hb[h] = lv[h] ? hist_base : hist_base + 1024u;
+      }
+      auto fill = [&](uint32_t s0, uint32_t buf) {
+#pragma unroll
+        for (int h = 0; h < kCPW; ++h) {
+          const uint4 w = gibbs_block(a.base + s0 + lane, a.stream_id + c0 + h, a);
+          su[p][buf][h][lane] = make_double2(u53_scaled(w.x, w.y), u53_scaled(w.z, w.w));
+        }
+      };
+      auto record = [&](uint32_t s0, uint32_t buf, uint32_t nb) {
         const uint32_t s = s0 + lane;
-        if (s >= a.burn_in) hist_inc(bin_addr_scaled(myX, hb));
-        if (STORE && live) {
-          if (a.out_x) a.out_x[(uint64_t)s * a.n_chains + c] = __dmul_rn(myX, kInvScale);
-          if (a.out_y) a.out_y[(uint64_t)s * a.n_chains + c] = __dmul_rn(myY, kInvScale);
+#pragma unroll
+        for (int h = 0; h < kCPW; ++h) {
+          if (!ex[h] || lane >= nb) continue;
+          const double2 st = sxy[p][buf][h][lane];
+          if (s >= a.burn_in) hist_inc(bin_addr_scaled(st.x, hb[h]));
+          if (STORE) {
+            const uint64_t o = (uint64_t)s * a.n_chains + c0 + h;
+            if (a.out_x) a.out_x[o] = lv[h] ? __dmul_rn(st.x, kInvScale) : qnan;
+            if (a.out_y) a.out_y[o] = lv[h] ? __dmul_rn(st.y, kInvScale) : qnan;
+          }
+        }
+      };
+      fill(0, 0);
+      pair_bar(p);
+      uint32_t bb = 0;
+      for (uint32_t s0 = 0; s0 < a.n_sweeps; s0 += 32, bb ^= 1) {
+        if (s0 + 32 < a.n_sweeps) fill(s0 + 32, bb ^ 1);
+        if (s0 >= 32) record(s0 - 32, bb ^ 1, 32);
+        pair_bar(p);
+      }
+      if (a.n_sweeps) {
+        const uint32_t sl = (a.n_sweeps - 1) & ~31u;
+        record(sl, (sl >> 5) & 1, a.n_sweeps - sl);
+      }
+    } else {
+      const uint32_t h = lane / kLPC;
+      const uint64_t c = c0 + h;
+      const bool ex = c < a.n_chains;
+      const bool rec = (lane % kLPC) == 0;
+      const double x0 = (ex && a.x0) ? a.x0[c] : 0.5;
+      const double y0 = (ex && a.y0) ? a.y0[c] : 0.5;
+      const bool live = ex && (y0 >= 0.0) && (y0 <= 1.0);
+      nbad += (rec && ex && !live);
+      WarpChain q;
+      q.X = __dmul_rn(x0, kScale);
+      q.Y = __dmul_rn(live ? y0 : qnan, kScale);
+      q.S1X = q.S2X = q.S1Y = q.S2Y = q.SXY = 0.0;
+      pair_bar(p);                               // batch 0's uniforms are in
+      uint32_t bb = 0;
+      for (uint32_t s0 = 0; s0 < a.n_sweeps; s0 += 32, bb ^= 1) {
+        const uint32_t nb = a.n_sweeps - s0 < 32u ? a.n_sweeps - s0 : 32u;
+        const double2* u = su[p][bb][h];
+        double2* xy = sxy[p][bb][h];
+        if (nb == 32 && s0 >= a.burn_in)
+          warp_batch<1, true>(q, u, xy, rec, nb, s0, a.burn_in);
+        else
+          warp_batch<2, false>(q, u, xy, rec, nb, s0, a.burn_in);
+        pair_bar(p);
+      }
+      if (ex) {
+        const double n = (double)(a.n_sweeps - a.burn_in);
+        const double nm1 = __dsub_rn(n, 1.0);
+        const double s1x = __dmul_rn(q.S1X, kInvScale), s1y = __dmul_rn(q.S1Y, kInvScale);
+        const double s2x = __dmul_rn(q.S2X, kInvScale2), s2y = __dmul_rn(q.S2Y, kInvScale2);
+        const double sxy_ = __dmul_rn(q.SXY, kInvScale2);
+        const double mx = __ddiv_rn(s1x, n), my = __ddiv_rn(s1y, n);
+        const double vx = __ddiv_rn(__dsub_rn(s2x, __dmul_rn(s1x, mx)), nm1);
+        const double vy = __ddiv_rn(__dsub_rn(s2y, __dmul_rn(s1y, my)), nm1);
+        const double cxy = __ddiv_rn(__dsub_rn(sxy_, __dmul_rn(s1x, my)), nm1);
+        if (rec) {
+          if (a.chain_stats) {
+            a.chain_stats[0 * a.n_chains + c] = mx;
+            a.chain_stats[1 * a.n_chains + c] = vx;
+            a.chain_stats[2 * a.n_chains + c] = my;
+            a.chain_stats[3 * a.n_chains + c] = vy;
+            a.chain_stats[4 * a.n_chains + c] = cxy;
+          }
+          if (a.final_xy) {
+            a.final_xy[c] = __dmul_rn(q.X, kInvScale);
+            a.final_xy[a.n_chains + c] = __dmul_rn(q.Y, kInvScale);
+          }
+          double* r = red[kCPW * p + h];
+          r[0] += mx; r[1] += vx; r[2] += mx * mx; r[3] += my;
+          r[4] += vy; r[5] += my * my; r[6] += cxy; r[7] += mx * my;
         }
       }
     }
-    // per-chain statistics (every lane holds them; lane 0 writes)
-    const double s1x = __dmul_rn(q.S1X, kInvScale), s1y = __dmul_rn(q.S1Y, kInvScale);
-    const double s2x = __dmul_rn(q.S2X, kInvScale2), s2y = __dmul_rn(q.S2Y, kInvScale2);
-    const double sxy = __dmul_rn(q.SXY, kInvScale2);
-    const double mx = __ddiv_rn(s1x, n), my = __ddiv_rn(s1y, n);
-    const double vx = __ddiv_rn(__dsub_rn(s2x, __dmul_rn(s1x, mx)), nm1);
-    const double vy = __ddiv_rn(__dsub_rn(s2y, __dmul_rn(s1y, my)), nm1);
-    const double cxy = __ddiv_rn(__dsub_rn(sxy, __dmul_rn(s1x, my)), nm1);
-    if (lane == 0) {
-      if (a.chain_stats) {
-        a.chain_stats[0 * a.n_chains + c] = mx;
-        a.chain_stats[1 * a.n_chains + c] = vx;
-        a.chain_stats[2 * a.n_chains + c] = my;
-        a.chain_stats[3 * a.n_chains + c] = vy;
-        a.chain_stats[4 * a.n_chains + c] = cxy;
-      }
-      if (a.final_xy) {
-        a.final_xy[c] = __dmul_rn(q.X, kInvScale);
-        a.final_xy[a.n_chains + c] = __dmul_rn(q.Y, kInvScale);
-      }
-      red[wid][0] += mx; red[wid][1] += vx; red[wid][2] += mx * mx; red[wid][3] += my;
-      red[wid][4] += vy; red[wid][5] += my * my; red[wid][6] += cxy; red[wid][7] += mx * my;
-    }
-    if (STORE && !live)                 // invalid start: NaN samples (oracle semantics)
-      for (uint32_t s = lane; s < a.n_sweeps; s += 32) {
-        if (a.out_x) a.out_x[(uint64_t)s * a.n_chains + c] = qnan;
-        if (a.out_y) a.out_y[(uint64_t)s * a.n_chains + c] = qnan;
-      }
   }
   __syncthreads();
   double* part = a.partials + (uint64_t)blockIdx.x * kTot;
   if (threadIdx.x < 8) {
     double v = 0.0;
-    for (int w = 0; w < kLatW; ++w) v += red[w][threadIdx.x];
+    for (int w = 0; w < kLatChains; ++w) v += red[w][threadIdx.x];
     part[threadIdx.x] = v;
   }
   for (int b = threadIdx.x; b < 256; b += kLatThreads) part[kHdr + b] = (double)hist[b];
@@ -536,11 +613,12 @@ int ctas_per_sm_small() {
   return cached;
 }
 int ctas_per_sm_lat() {
-  static int cached = occupancy(gibbs_warp_kernel<true>, kLatThreads);
+  static int cached = occupancy(gibbs_lat_kernel<true>, kLatThreads);
   return cached;
 }
-// Latency mode (one warp per chain) for chain counts up to this many per SM:
-// below it a warp per chain finishes sooner than a thread per chain (cfg1:
+// Latency mode (chain/helper warp pairs) for chain counts up to this many per SM:
+// below it the chain/helper warp pairs finish sooner than a thread per chain
+// (4736 chains: 58 vs 91 us, 9472: 102 vs 91 us; tools/lat_probe.py) (cfg1:
 // 1024 chains).
 #ifndef BRNG_GIBBS_LAT_PER_SM
 #define BRNG_GIBBS_LAT_PER_SM 32
@@ -611,13 +689,13 @@ cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
   a.c3k1_u = (uint32_t)(ctx.stream_id >> 32) ^ a.rk1[0];
   unsigned n_parts = grid;
   if (n_chains <= (uint64_t)ctx.num_sms * BRNG_GIBBS_LAT_PER_SM) {
-    const uint64_t want = (n_chains + kLatW - 1) / kLatW;
+    const uint64_t want = (n_chains + kLatChains - 1) / kLatChains;
     const uint64_t cap = (uint64_t)ctx.num_sms * ctas_per_sm_lat();
     n_parts = (unsigned)(want < cap ? (want ? want : 1) : cap);
     if (store)
-      gibbs_warp_kernel<true><<<n_parts, kLatThreads, 0, ctx.stream>>>(a);
+      gibbs_lat_kernel<true><<<n_parts, kLatThreads, 0, ctx.stream>>>(a);
     else
-      gibbs_warp_kernel<false><<<n_parts, kLatThreads, 0, ctx.stream>>>(a);
+      gibbs_lat_kernel<false><<<n_parts, kLatThreads, 0, ctx.stream>>>(a);
   } else if (sh.small) {
     if (store)
       gibbs_kernel<true, kSmallCPT, kSmallThreads, false><<<grid, kSmallThreads, 0, ctx.stream>>>(a);

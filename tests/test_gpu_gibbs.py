@@ -157,16 +157,16 @@ def test_host_pipeline_multi_chunk_gibbs():
 
 
 def test_launch_shapes_agree_across_the_latency_threshold():
-    """Three launch shapes serve different chain counts (warp per chain up to
-    32 chains per SM, thread per chain below half a bulk wave, two chains per
-    thread above).  A chain's samples, statistics and final state must not
-    depend on which one ran it: chains 0..n-1 of a run just above the
-    warp-per-chain threshold equal the same chains of a run just below it,
+    """Three launch shapes serve different chain counts (chain/helper warp
+    pairs up to 32 chains per SM, thread per chain below half a bulk wave,
+    three chains per thread above).  A chain's samples, statistics and final
+    state must not depend on which one ran it: chains 0..n-1 of a run just
+    above the latency-mode threshold equal the same chains of a run just below it,
     and both equal the oracle on sampled chains; histograms are exact."""
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     thr = 32 * sms                          # BRNG_GIBBS_LAT_PER_SM (gibbs.cu)
     ns, burn = 40, 3
-    lo = _run(42, 5, 1000, thr, ns, burn)            # warp per chain
+    lo = _run(42, 5, 1000, thr, ns, burn)            # chain/helper warp pairs
     hi = _run(42, 5, 1000, thr + 37, ns, burn)       # thread per chain
     for k in ("out_x", "out_y"):
         assert np.array_equal(lo[k], hi[k][:, :thr]), k
