@@ -342,7 +342,9 @@ def gpu_arm(args):
         ms = tt.item()
     ms_step = ms / args.steps
     step_ms = [marks[k].elapsed_time(marks[k + 1]) for k in range(args.steps)]
-    per = {n: statistics.mean(e[n][0].elapsed_time(e[n][1]) for e in evs) for n in names}
+    # per-row device times: median over the timed steps (the first step's
+    # first row also contains the host's enqueue latency after the idle sync)
+    per = {n: statistics.median(e[n][0].elapsed_time(e[n][1]) for e in evs) for n in names}
     # determinism: the outputs of the last timed step vs one more (untimed) step
     # (cfg5 totals include the all-reduce, so they are compared at N = 1 only)
     cs_a = wl.checksums()
