@@ -194,3 +194,24 @@ def test_bulk_launch_high_stream_word(stream_id):
         assert np.array_equal(g["out_x"][:, c], r["out_x"][:, 0]), c
         assert np.array_equal(g["out_y"][:, c], r["out_y"][:, 0]), c
         assert np.array_equal(g["chain_stats"][:, c], r["chain_stats"][:, 0]), c
+
+
+@pytest.mark.parametrize("n_chains", [5, 4_737 + 3, 160_001])   # latency / small / bulk shapes
+@pytest.mark.parametrize("n_sweeps,burn", [(0, 0), (4, 4), (33, 33)])
+def test_degenerate_sweep_counts(n_chains, n_sweeps, burn):
+    """No sweeps, or every sweep burnt in: no statistics samples (NaN
+    moments, empty histogram), final state = start state (or the chain after
+    its sweeps), cursor advanced by n_sweeps - the oracle's results, in
+    every launch shape."""
+    g = _run(3, 11, 5, n_chains, n_sweeps, burn, samples=n_sweeps > 0)
+    cols = np.unique(np.array([0, 1, n_chains // 2, n_chains - 1]))
+    r = oracle.gibbs_triangle(3, 11, 5, 1, n_sweeps, burn_in=burn)      # chain 0 only
+    assert np.array_equal(g["final_xy"][:, :1], r["final_xy"], equal_nan=True)
+    assert np.isnan(g["chain_stats"]).all()
+    assert g["totals"][HDR:].sum() == 0
+    assert g["totals"][8] == n_chains and g["totals"][9] == 0
+    for c in cols:
+        rc = oracle.gibbs_triangle(3, 11 + int(c), 5, 1, n_sweeps, burn_in=burn)
+        assert np.array_equal(g["final_xy"][:, c], rc["final_xy"][:, 0]), c
+        if n_sweeps:
+            assert np.array_equal(g["out_x"][:, c], rc["out_x"][:, 0]), c
