@@ -92,6 +92,8 @@ typedef enum brng_status {
 /* ---- lifecycle (the paper's constructor / destructor) ---------- */
 
 /* Create a handle bound to the CURRENT CUDA device, cursor 0, default stream.
+ * Every later call runs on that device whatever device is current in the
+ * calling thread, and leaves the caller's current device unchanged.
  * seed: Philox key (any value, including 0).  stream_id: Philox stream (upper
  * counter half) used by every fill/Gamma/Dirichlet call; Gibbs chain c uses
  * stream stream_id + c.  *out receives the handle.  Allocates ~4 KB device

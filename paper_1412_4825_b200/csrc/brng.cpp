@@ -74,15 +74,36 @@ Ctx make_ctx(brng_t h) {
   return c;
 }
 
-int check_device(brng_t h) {
-  int dev = -1;
-  if (cudaGetDevice(&dev) != cudaSuccess) return BRNG_ERR_CUDA;
-  if (dev != h->device) {
-    // Launch on the handle's device regardless of the caller's current device.
-    if (cudaSetDevice(h->device) != cudaSuccess) return BRNG_ERR_STATE;
+// Makes the handle's device current for one C-ABI call and restores the
+// caller's current device when the call returns (the library never leaves a
+// different device current behind).
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(brng_t h) {
+    if (cudaGetDevice(&prev_) != cudaSuccess) {
+      status_ = BRNG_ERR_CUDA;
+      return;
+    }
+    if (prev_ != h->device) {
+      if (cudaSetDevice(h->device) != cudaSuccess) {
+        status_ = BRNG_ERR_STATE;
+        return;
+      }
+      changed_ = true;
+    }
   }
-  return BRNG_OK;
-}
+  ~DeviceGuard() {
+    if (changed_) cudaSetDevice(prev_);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+  int status() const { return status_; }
+
+ private:
+  int prev_ = -1;
+  bool changed_ = false;
+  int status_ = BRNG_OK;
+};
 
 // span = ceil(n / per) * mult with overflow checks; cursor + span <= 2^64.
 int reserve(brng_t h, uint64_t n, uint64_t per, uint64_t mult, uint64_t* base) {
@@ -263,7 +284,8 @@ int fill_common(brng_t h, int dist, int dtype, const void* p0, const void* p1, v
   if (dist == brng::kExponential && !p0) return BRNG_ERR_NULL;
   if (n == 0) return BRNG_OK;
   if (!mul_ok(n, esize)) return BRNG_ERR_SIZE;
-  int st = check_device(h);
+  DeviceGuard dg(h);
+  int st = dg.status();
   if (st) return st;
   const uint64_t per = (uint64_t)brng::samples_per_block(dist, dtype);
   uint64_t base;
@@ -287,7 +309,8 @@ int batch_common(brng_t h, int dist, int dtype, double p0, double p1, void* out,
   if (n == 0) return BRNG_OK;
   const size_t esize = dtype == brng::kF64 ? 8 : 4;
   if (!mul_ok(n, esize)) return BRNG_ERR_SIZE;
-  int st = check_device(h);
+  DeviceGuard dg(h);
+  int st = dg.status();
   if (st) return st;
   const uint64_t per = (uint64_t)brng::samples_per_block(dist, dtype);
   uint64_t base;
@@ -308,7 +331,8 @@ int gamma_common(brng_t h, int dtype, const void* alpha, const void* beta, void*
   if (!h || !alpha || !beta || !out) return BRNG_ERR_NULL;
   if (n == 0) return BRNG_OK;
   if (!mul_ok(n, esize)) return BRNG_ERR_SIZE;
-  int st = check_device(h);
+  DeviceGuard dg(h);
+  int st = dg.status();
   if (st) return st;
   uint64_t base;
   if ((st = reserve(h, n, 1, BRNG_GAMMA_STRIDE, &base))) return st;
@@ -332,7 +356,8 @@ int dirichlet_common(brng_t h, int dtype, const void* alpha, uint64_t n_rows, ui
   if (!mul_ok(n_rows, k)) return BRNG_ERR_SIZE;
   const uint64_t n = n_rows * k;
   if (!mul_ok(n, esize)) return BRNG_ERR_SIZE;
-  int st = check_device(h);
+  DeviceGuard dg(h);
+  int st = dg.status();
   if (st) return st;
   uint64_t base;
   if ((st = reserve(h, n, 1, BRNG_GAMMA_STRIDE, &base))) return st;
@@ -390,7 +415,7 @@ int brng_create(uint64_t seed, uint64_t stream_id, brng_t* out) {
 
 int brng_destroy(brng_t h) {
   if (!h) return BRNG_ERR_NULL;
-  cudaSetDevice(h->device);
+  DeviceGuard dg(h);
   cudaStreamSynchronize(h->stream);
   cudaFree(h->d_err);
   if (h->d_partials) cudaFree(h->d_partials);
@@ -434,10 +459,14 @@ int brng_get_key(brng_t h, uint64_t* seed, uint64_t* stream_id) {
 }
 int brng_synchronize(brng_t h) {
   if (!h) return BRNG_ERR_NULL;
+  DeviceGuard dg(h);
+  if (dg.status()) return dg.status();
   return cuda_status(cudaStreamSynchronize(h->stream));
 }
 int brng_device_errors(brng_t h, uint64_t* n) {
   if (!h || !n) return BRNG_ERR_NULL;
+  DeviceGuard dg(h);
+  if (dg.status()) return dg.status();
   unsigned long long v = 0;
   cudaError_t e = cudaMemcpyAsync(&v, h->d_err, sizeof(v), cudaMemcpyDeviceToHost, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
@@ -446,6 +475,8 @@ int brng_device_errors(brng_t h, uint64_t* n) {
 }
 int brng_reset_device_errors(brng_t h) {
   if (!h) return BRNG_ERR_NULL;
+  DeviceGuard dg(h);
+  if (dg.status()) return dg.status();
   return cuda_status(cudaMemsetAsync(h->d_err, 0, sizeof(unsigned long long), h->stream));
 }
 
@@ -529,7 +560,8 @@ int brng_gibbs_triangle(brng_t h, uint64_t n_chains, uint64_t n_sweeps, const do
   if (!mul_ok(n_chains, n_sweeps) || !mul_ok(n_chains * n_sweeps, 8) || !mul_ok(n_chains, 40))
     return BRNG_ERR_SIZE;
   if (n_chains > std::numeric_limits<uint64_t>::max() - h->stream_id) return BRNG_ERR_OVERFLOW;
-  int st = check_device(h);
+  DeviceGuard dg(h);
+  int st = dg.status();
   if (st) return st;
   uint64_t base;
   if ((st = reserve(h, n_sweeps, 1, 1, &base))) return st;
