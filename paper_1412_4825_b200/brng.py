@@ -76,8 +76,13 @@ class BrngError(RuntimeError):
         super().__init__(f"{fn}: {brng_status_string(status)} ({status})")
 
 
-def _ptr(x):
-    """torch.Tensor / numpy array / int / None -> address (no copies)."""
+def _ptr(x, itemsize=None, count=None):
+    """torch.Tensor / numpy array / int / None -> address (no copies).
+
+    For tensors and arrays the element size and length are checked against
+    what the C call will touch (itemsize bytes x count elements), so a wrong
+    dtype or a short array raises instead of corrupting memory.  Raw integer
+    addresses are passed through unchecked."""
     if x is None:
         return None
     if isinstance(x, int):
@@ -86,13 +91,19 @@ def _ptr(x):
     if dp is not None:
         if not x.is_contiguous():
             raise ValueError("brng: arrays must be contiguous")
-        return dp()
-    ct = getattr(x, "ctypes", None)
-    if ct is not None:
+        size, length, addr = x.element_size(), x.numel(), dp()
+    else:
+        ct = getattr(x, "ctypes", None)
+        if ct is None:
+            raise TypeError(f"brng: unsupported array type {type(x)}")
         if not x.flags["C_CONTIGUOUS"]:
             raise ValueError("brng: arrays must be contiguous")
-        return ct.data
-    raise TypeError(f"brng: unsupported array type {type(x)}")
+        size, length, addr = x.itemsize, x.size, ct.data
+    if itemsize is not None and size != itemsize:
+        raise TypeError(f"brng: expected {itemsize}-byte elements, got {size}-byte")
+    if count is not None and length < count:
+        raise ValueError(f"brng: array of {length} elements, the call needs {count}")
+    return addr
 
 
 def _check(fn, st):
@@ -154,7 +165,8 @@ def brng_synchronize(h) -> int:
 
 
 def _fill(name, h, n, *arrays):
-    return _check(name, getattr(_lib, name)(h, *[_ptr(a) for a in arrays], n))
+    size = 8 if name.endswith("f64") else 4
+    return _check(name, getattr(_lib, name)(h, *[_ptr(a, size, n) for a in arrays], n))
 
 
 def brng_raw_u32(h, out, n):
@@ -199,7 +211,9 @@ DTYPE = {"f32": 0, "f64": 1}
 
 def brng_batch_fill(h, dist, dtype, p0, p1, out, n):
     """Fixed-parameter fill; dist/dtype are the BRNG_DIST_*/BRNG_DTYPE_* codes."""
-    return _check("brng_batch_fill", _lib.brng_batch_fill(h, dist, dtype, p0, p1, _ptr(out), n))
+    size = 8 if dtype == DTYPE["f64"] else 4
+    return _check("brng_batch_fill", _lib.brng_batch_fill(h, dist, dtype, p0, p1,
+                                                          _ptr(out, size, n), n))
 
 
 def brng_log_uniform_f32(h, out, n):
@@ -227,30 +241,34 @@ def brng_weibull_f64(h, alpha, beta, out, n):
 
 
 def brng_gamma_f32(h, alpha, beta, out, n, trials=None):
-    return _check("brng_gamma_f32", _lib.brng_gamma_f32(h, _ptr(alpha), _ptr(beta), _ptr(out),
-                                                        n, _ptr(trials)))
+    return _check("brng_gamma_f32", _lib.brng_gamma_f32(
+        h, _ptr(alpha, 4, n), _ptr(beta, 4, n), _ptr(out, 4, n), n, _ptr(trials, 1, n)))
 
 
 def brng_gamma_f64(h, alpha, beta, out, n, trials=None):
-    return _check("brng_gamma_f64", _lib.brng_gamma_f64(h, _ptr(alpha), _ptr(beta), _ptr(out),
-                                                        n, _ptr(trials)))
+    return _check("brng_gamma_f64", _lib.brng_gamma_f64(
+        h, _ptr(alpha, 8, n), _ptr(beta, 8, n), _ptr(out, 8, n), n, _ptr(trials, 1, n)))
 
 
 def brng_dirichlet_f32(h, alpha, n_rows, k, out, trials=None):
-    return _check("brng_dirichlet_f32", _lib.brng_dirichlet_f32(h, _ptr(alpha), n_rows, k,
-                                                                _ptr(out), _ptr(trials)))
+    m = n_rows * k
+    return _check("brng_dirichlet_f32", _lib.brng_dirichlet_f32(
+        h, _ptr(alpha, 4, m), n_rows, k, _ptr(out, 4, m), _ptr(trials, 1, m)))
 
 
 def brng_dirichlet_f64(h, alpha, n_rows, k, out, trials=None):
-    return _check("brng_dirichlet_f64", _lib.brng_dirichlet_f64(h, _ptr(alpha), n_rows, k,
-                                                                _ptr(out), _ptr(trials)))
+    m = n_rows * k
+    return _check("brng_dirichlet_f64", _lib.brng_dirichlet_f64(
+        h, _ptr(alpha, 8, m), n_rows, k, _ptr(out, 8, m), _ptr(trials, 1, m)))
 
 
 def brng_gibbs_triangle(h, n_chains, n_sweeps, x0=None, y0=None, burn_in=0, out_x=None,
                         out_y=None, chain_stats=None, final_xy=None, totals=None):
+    c, s = n_chains, n_chains * n_sweeps
     return _check("brng_gibbs_triangle", _lib.brng_gibbs_triangle(
-        h, n_chains, n_sweeps, _ptr(x0), _ptr(y0), burn_in, _ptr(out_x), _ptr(out_y),
-        _ptr(chain_stats), _ptr(final_xy), _ptr(totals)))
+        h, n_chains, n_sweeps, _ptr(x0, 8, c), _ptr(y0, 8, c), burn_in, _ptr(out_x, 8, s),
+        _ptr(out_y, 8, s), _ptr(chain_stats, 8, 5 * c), _ptr(final_xy, 8, 2 * c),
+        _ptr(totals, 8, TOTALS_LEN)))
 
 
 def raw_call(name, *args):

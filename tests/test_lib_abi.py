@@ -76,6 +76,26 @@ def test_host_validation_without_launch():
     assert raw("brng_create", 1, 0, None) == -1
 
 
+def test_binding_checks_element_size_and_length():
+    """The binding refuses arrays whose dtype or length does not match what
+    the C call would touch (no memory corruption from a wrong tensor)."""
+    import numpy as np
+    import paper_1412_4825_b200 as B
+    p = B.brng._ptr
+    a = np.zeros(8)
+    assert p(a, 8, 8) == a.ctypes.data and p(None, 8, 8) is None and p(1234, 8, 8) == 1234
+    with pytest.raises(TypeError):
+        p(np.zeros(8, np.float32), 8, 8)            # f32 array for an f64 call
+    with pytest.raises(ValueError):
+        p(a, 8, 9)                                  # too short
+    with pytest.raises(ValueError):
+        p(np.zeros((4, 4))[:, ::2], 8, 4)           # not contiguous
+    with pytest.raises(TypeError):                  # before any C call (no GPU needed)
+        B.brng_gaussian_f64(1, np.zeros(4, np.float32), np.zeros(4), np.zeros(4), 4)
+    with pytest.raises(ValueError):
+        B.brng_gibbs_triangle(1, 10, 3, totals=np.zeros(B.TOTALS_LEN - 1))
+
+
 def test_create_without_gpu_reports_cuda_error():
     import torch
     if torch.cuda.is_available():
