@@ -71,6 +71,7 @@ Ctx make_ctx(brng_t h) {
   c.k1 = (uint32_t)(h->seed >> 32);
   c.stream_id = h->stream_id;
   c.err = h->d_err;
+  c.work = h->d_err + 1;
   return c;
 }
 
@@ -404,8 +405,8 @@ int brng_create(uint64_t seed, uint64_t stream_id, brng_t* out) {
   h->device = dev; h->num_sms = sms; h->stream = nullptr;
   h->d_partials = nullptr; h->partials_cap = 0; h->d_totals = nullptr;
   h->pipe_ready = false; h->stage_cap = 0;
-  if (cudaMalloc(&h->d_err, sizeof(unsigned long long)) != cudaSuccess ||
-      cudaMemset(h->d_err, 0, sizeof(unsigned long long)) != cudaSuccess) {
+  if (cudaMalloc(&h->d_err, 2 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMemset(h->d_err, 0, 2 * sizeof(unsigned long long)) != cudaSuccess) {
     delete h;
     return BRNG_ERR_CUDA;
   }

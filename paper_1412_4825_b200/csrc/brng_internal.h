@@ -18,6 +18,7 @@ struct Ctx {
   uint32_t k0, k1;           // Philox key = (lo32 seed, hi32 seed)
   uint64_t stream_id;        // Philox stream of fills / Gamma / Dirichlet
   unsigned long long* err;   // device invalid-sample counter
+  unsigned long long* work;  // device work counter (dynamic chunk assignment)
 };
 
 // K1/K2: raw words, standard uniforms and per-sample-parameter transforms.

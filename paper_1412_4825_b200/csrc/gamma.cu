@@ -23,12 +23,13 @@ namespace {
 
 constexpr int kThreads = 256;
 // Samples per warp queue (Gamma): a queue's tail (lanes idle while its last
-// samples finish) happens once per chunk.  512 / 1024 / 2048 / 4096 samples
-// measured 0.949 / 0.932 / 0.913 / 0.877 ms on cfg3; one chunk per warp of a
-// single resident wave (~14k) 0.974 (no CTAs left to fill the SMs that
-// finish first).
+// samples finish) happens once per chunk.  Warps take chunks from a device
+// counter (BRNG_GAMMA_DYN, one resident wave of CTAs), so the kernel's tail is
+// at most one chunk per warp: cfg3 0.877 ms with a static grid-stride
+// assignment of 4096-sample chunks -> 0.840 (2048, dynamic), 0.846 (4096,
+// dynamic), 0.837 (1024, dynamic); Dirichlet row groups likewise 4.48 -> 4.33.
 #ifndef BRNG_GAMMA_CHUNK
-#define BRNG_GAMMA_CHUNK 4096
+#define BRNG_GAMMA_CHUNK 2048
 #endif
 constexpr uint64_t kChunk = BRNG_GAMMA_CHUNK;
 constexpr uint32_t kStride = 256;          // blocks per sample (R-11)
@@ -160,8 +161,15 @@ struct GammaArgs {
   uint64_t n, base, stream;
   RoundKeys rk;
   unsigned long long* err;
+  unsigned long long* work;
 };
 
+// Dynamic chunk / row-group assignment: a warp's lane 0 takes the next index
+// from the handle's work counter (zeroed by a memset before each launch).
+// The values never depend on which warp ran a chunk.
+#ifndef BRNG_GAMMA_DYN
+#define BRNG_GAMMA_DYN 1
+#endif
 template <typename T>
 #ifndef BRNG_GAMMA_MINB
 #define BRNG_GAMMA_MINB 4
@@ -173,7 +181,17 @@ __global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(const 
   const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   const uint64_t n_warps = ((uint64_t)gridDim.x * kThreads) >> 5;
   uint32_t nbad = 0;
+#if BRNG_GAMMA_DYN
+  (void)warp; (void)n_warps;
+  for (;;) {
+    unsigned long long cidx = 0;
+    if ((threadIdx.x & 31) == 0) cidx = atomicAdd(a.work, 1ull);
+    cidx = __shfl_sync(kFull, cidx, 0);
+    const uint64_t beg = (uint64_t)cidx * kChunk;
+    if (beg >= a.n) break;
+#else
   for (uint64_t beg = warp * kChunk; beg < a.n; beg += n_warps * kChunk) {
+#endif
     const uint64_t end = beg + kChunk < a.n ? beg + kChunk : a.n;
     mt_queue(
         beg, end, a.base, a.rk, tb,
@@ -199,6 +217,7 @@ struct DirArgs {
   RoundKeys rk;
   unsigned long long* err;
   uint32_t rpw;          // rows per warp queue (smem kernel)
+  unsigned long long* work;   // dynamic group counter (BRNG_GAMMA_DYN)
 };
 
 constexpr int kDirThreads = 128;     // 4 warps / CTA, one row per warp
@@ -232,7 +251,16 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __gri
   const uint64_t n_warps = ((uint64_t)gridDim.x * kDirThreads) >> 5;
   const uint64_t n_groups = (a.n_rows + a.rpw - 1) / a.rpw;
   uint32_t nbad = 0;
+#if BRNG_GAMMA_DYN
+  (void)warp; (void)n_warps;
+  for (;;) {
+    unsigned long long gidx = 0;
+    if (lane == 0) gidx = atomicAdd(a.work, 1ull);
+    const uint64_t grp = __shfl_sync(kFull, gidx, 0);
+    if (grp >= n_groups) break;
+#else
   for (uint64_t grp = warp; grp < n_groups; grp += n_warps) {
+#endif
     const uint64_t row0 = grp * a.rpw;
     const uint64_t rows = a.n_rows - row0 < a.rpw ? a.n_rows - row0 : a.rpw;
     const uint64_t beg = row0 * a.k;
@@ -296,10 +324,20 @@ template <typename T>
 cudaError_t gamma_typed(const T* alpha, const T* beta, T* out, uint8_t* trials, uint64_t n,
                         uint64_t base, const Ctx& ctx) {
   GammaArgs<T> a{alpha, beta, out, trials, n, base, ctx.stream_id,
-                   make_round_keys(ctx.k0, ctx.k1, ctx.stream_id), ctx.err};
+                   make_round_keys(ctx.k0, ctx.k1, ctx.stream_id), ctx.err, ctx.work};
+#if BRNG_GAMMA_DYN
+  {
+    cudaError_t e = cudaMemsetAsync(ctx.work, 0, sizeof(unsigned long long), ctx.stream);
+    if (e != cudaSuccess) return e;
+  }
+#endif
   const uint64_t warps_needed = (n + kChunk - 1) / kChunk;
   const uint64_t ctas_needed = (warps_needed + (kThreads / 32) - 1) / (kThreads / 32);
+#if BRNG_GAMMA_DYN
+  const uint64_t cap = (uint64_t)ctx.num_sms * BRNG_GAMMA_MINB;   // one resident wave
+#else
   const uint64_t cap = (uint64_t)ctx.num_sms * 8;  // two waves of 4 resident CTAs/SM
+#endif
   const unsigned g = (unsigned)(ctas_needed < cap ? ctas_needed : cap);
   gamma_kernel<T><<<g, kThreads, 0, ctx.stream>>>(a);
   return cudaGetLastError();
@@ -309,7 +347,7 @@ template <typename T>
 cudaError_t dirichlet_typed(const T* alpha, uint64_t n_rows, uint64_t k, T* out,
                             uint8_t* trials, uint64_t base, const Ctx& ctx) {
   DirArgs<T> a{alpha, out, trials, n_rows, k, base, ctx.stream_id,
-                 make_round_keys(ctx.k0, ctx.k1, ctx.stream_id), ctx.err, 1u};
+                 make_round_keys(ctx.k0, ctx.k1, ctx.stream_id), ctx.err, 1u, ctx.work};
   const uint64_t ctas_needed = (n_rows + 3) / 4;
   if (k <= kDirSmemK) {
     const uint64_t r = kDirTarget / k;
@@ -323,7 +361,19 @@ cudaError_t dirichlet_typed(const T* alpha, uint64_t n_rows, uint64_t k, T* out,
     }
     const uint64_t groups = (n_rows + a.rpw - 1) / a.rpw;
     const uint64_t ctas = (groups + 3) / 4;
+#if BRNG_GAMMA_DYN
+    // one resident wave of CTAs; warps take row groups from a counter
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dirichlet_smem_kernel<T>,
+                                                      kDirThreads, smem) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    const uint64_t cap = (uint64_t)ctx.num_sms * per_sm;
+    cudaError_t e0 = cudaMemsetAsync(ctx.work, 0, sizeof(unsigned long long), ctx.stream);
+    if (e0 != cudaSuccess) return e0;
+#else
     const uint64_t cap = (uint64_t)ctx.num_sms * 16 * 8;
+#endif
     const unsigned g = (unsigned)(ctas < cap ? ctas : cap);
     dirichlet_smem_kernel<T><<<g, kDirThreads, smem, ctx.stream>>>(a);
   } else {
