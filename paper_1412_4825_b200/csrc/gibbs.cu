@@ -348,12 +348,22 @@ gibbs_kernel(GibbsArgs a) {
 // of the ~22 us of one thread walking all rows with dependent L2 loads).
 // accumulate != 0: add to totals (a host-staged call processed in chunks).
 constexpr int kRedThreads = 256;
+// K7 as a programmatic dependent launch (its launch overlaps the Gibbs
+// kernel's tail instead of following it).
+#ifndef BRNG_K7_PDL
+#define BRNG_K7_PDL 1
+#endif
 __global__ void __launch_bounds__(kRedThreads) reduce_partials_kernel(const double* partials,
                                                                      uint32_t n_parts,
                                                                      double* totals,
                                                                      double n_chains,
                                                                      double n_samples,
                                                                      int accumulate) {
+#if BRNG_K7_PDL
+  // launched as a programmatic dependent of the Gibbs kernel: wait here until
+  // that grid has completed and its partials are visible
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t j = blockIdx.x * (kRedThreads / 32) + (threadIdx.x >> 5);
   if (j >= (uint32_t)kTot) return;
@@ -714,11 +724,26 @@ cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || totals == nullptr) return e;
+  const double n_samples = (double)n_chains * (double)(n_sweeps - burn_in);
+  const int acc = accumulate ? 1 : 0;
+#if BRNG_K7_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((kTot + kRedThreads / 32 - 1) / (kRedThreads / 32));
+  cfg.blockDim = dim3(kRedThreads);
+  cfg.stream = ctx.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, reduce_partials_kernel, (const double*)partials, n_parts, totals,
+                            (double)n_chains, n_samples, acc);
+#else
   reduce_partials_kernel<<<(kTot + kRedThreads / 32 - 1) / (kRedThreads / 32), kRedThreads, 0,
-                           ctx.stream>>>(
-      partials, n_parts, totals, (double)n_chains, (double)n_chains * (double)(n_sweeps - burn_in),
-      accumulate ? 1 : 0);
+                           ctx.stream>>>(partials, n_parts, totals, (double)n_chains, n_samples,
+                                         acc);
   return cudaGetLastError();
+#endif
 }
 
 }  // namespace brng
