@@ -2,6 +2,10 @@
 // clock64 around N dependent ops): the constants of the Gibbs latency
 // roofline (cfg1).  nvcc -O3 -gencode arch=compute_100a,code=sm_100a
 // tools/ulat.cu -o /tmp/ulat && /tmp/ulat
+// Caveat: the loops are fully unrolled over N = 4096 steps, so the multi-op
+// modes (stats, lagged stats, LDS ring, records) run from a code footprint far
+// beyond the instruction cache and overstate their cost; tools/ulat2.cu
+// measures the same bodies 32-unrolled as the kernels run them.
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
