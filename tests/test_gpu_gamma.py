@@ -230,3 +230,25 @@ def test_dirichlet_beyond_2_31_components():
     _assert_decisions(tot, "dirichlet > 2^31")
     del alpha, out, tr
     torch.cuda.empty_cache()
+
+
+def test_gamma_extreme_shapes():
+    """Shapes at the ends of binary64: tiny and subnormal alpha (the boost
+    underflows to 0 unless ln(1-u) = 0), huge alpha, infinite alpha
+    (invalid); each matches the oracle's decisions and values."""
+    alpha = torch.tensor([1e-300, 5e-324, 1e-20, 1e-8, 1e15, 1e300, float("inf"), 0.5],
+                         dtype=torch.float64)
+    beta = torch.tensor([1.0, 1.0, 3.0, 1.0, 1e-10, 1.0, 1.0, 1e100], dtype=torch.float64)
+    alpha = alpha.repeat(64)                      # several trials/boost blocks per shape
+    beta = beta.repeat(64)
+    n = len(alpha)
+    with handle(17, 3, 5) as h:
+        out = torch.empty(n, dtype=torch.float64, device=dev())
+        tr = torch.empty(n, dtype=torch.uint8, device=dev())
+        B.brng_gamma_f64(h, alpha.to(dev()), beta.to(dev()), out, n, tr)
+        assert B.brng_device_errors(h) == 64       # alpha = inf
+    r = parity.gamma_compare(out, tr, alpha.numpy(), beta.numpy(), 17, 3, 5)
+    _assert_decisions(r, "extreme shapes")
+    o = out.cpu().numpy().reshape(64, 8)
+    assert np.isnan(o[:, 6]).all()
+    assert np.all(o[:, [0, 1, 2]] >= 0) and np.all(np.isfinite(o[:, [0, 1, 2, 3, 4, 5, 7]]))
