@@ -289,8 +289,12 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __gri
   flush_errors(a.err, nbad);
 }
 
-// Any K: two passes over the row's Gamma samples (the second recomputes them
-// from their counters -- exact, no scratch).
+// Any K: two passes over the row.  binary64 output: the first pass stores the
+// unnormalised Gammas in the output row itself, the second rescales them in
+// place (the same values as the shared-memory kernel).  binary32 output: a
+// Gamma may not be representable in binary32 before the division (a row of
+// tiny alphas), so the second pass recomputes it from its counters -- exact,
+// no scratch.
 template <typename T>
 __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(const __grid_constant__ DirArgs<T> a) {
   __shared__ BoostItem qs[kDirThreads / 32][kBoostCap];
@@ -306,16 +310,31 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(const __gr
       be = 1.0;
     };
     double s = 0.0;
-    mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
-             [&](uint64_t, double v, uint32_t) { s += v; }, nbad, q);
-    s = warp_sum(s);
-    const double inv = 1.0 / s;
-    mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
-             [&](uint64_t i, double v, uint32_t t) {
-               a.out[i] = (T)(v * inv);
-               if (a.trials) a.trials[i] = (uint8_t)t;
-             },
-             nbad2, q);
+    if constexpr (sizeof(T) == 8) {
+      mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
+               [&](uint64_t i, double v, uint32_t t) {
+                 s += v;
+                 a.out[i] = (T)v;
+                 if (a.trials) a.trials[i] = (uint8_t)t;
+               },
+               nbad, q);
+      s = warp_sum(s);
+      const double inv = 1.0 / s;
+      __syncwarp();                           // the row's stores are visible to the warp
+      const uint32_t lane = threadIdx.x & 31;
+      for (uint64_t j = lane; j < a.k; j += 32) a.out[beg + j] = (T)((double)a.out[beg + j] * inv);
+    } else {
+      mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
+               [&](uint64_t, double v, uint32_t) { s += v; }, nbad, q);
+      s = warp_sum(s);
+      const double inv = 1.0 / s;
+      mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
+               [&](uint64_t i, double v, uint32_t t) {
+                 a.out[i] = (T)(v * inv);
+                 if (a.trials) a.trials[i] = (uint8_t)t;
+               },
+               nbad2, q);
+    }
   }
   flush_errors(a.err, nbad);
 }
