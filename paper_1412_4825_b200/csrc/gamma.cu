@@ -221,7 +221,10 @@ struct DirArgs {
 };
 
 constexpr int kDirThreads = 128;     // 4 warps / CTA, one row per warp
-constexpr uint64_t kDirSmemK = 2048; // rows up to this K are staged in smem
+#ifndef BRNG_DIR_SMEM_K
+#define BRNG_DIR_SMEM_K 2048
+#endif
+constexpr uint64_t kDirSmemK = BRNG_DIR_SMEM_K;   // rows up to this K are staged in smem
 #ifndef BRNG_DIR_TARGET
 #define BRNG_DIR_TARGET 512
 #endif
@@ -368,7 +371,11 @@ cudaError_t dirichlet_typed(const T* alpha, uint64_t n_rows, uint64_t k, T* out,
   DirArgs<T> a{alpha, out, trials, n_rows, k, base, ctx.stream_id,
                  make_round_keys(ctx.k0, ctx.k1, ctx.stream_id), ctx.err, 1u, ctx.work};
   const uint64_t ctas_needed = (n_rows + 3) / 4;
-  if (k <= kDirSmemK) {
+  // binary64 output parks the row's Gammas in the output row instead (no
+  // shared-memory occupancy cost): faster from K = 1024 on (tools/dirichlet_k.py:
+  // 2^27 components, K = 1024: 2.38 -> 2.12 ms, K = 2048: 3.71 -> 2.10 ms)
+  const uint64_t smem_k = sizeof(T) == 8 ? (kDirSmemK < 512 ? kDirSmemK : 512) : kDirSmemK;
+  if (k <= smem_k) {
     const uint64_t r = kDirTarget / k;
     a.rpw = (uint32_t)(r < 1 ? 1 : (r > 8 ? 8 : r));
     const size_t smem = (size_t)4 * a.rpw * k * sizeof(double);

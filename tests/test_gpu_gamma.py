@@ -114,7 +114,7 @@ def test_cfg3_full_size_sampled():
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("rows,k", [(1, 1), (3, 2), (257, 256), (64, 37), (33, 300),
-                                    (5, 2049), (2, 5000)])
+                                    (9, 700), (5, 2049), (2, 5000)])
 def test_dirichlet_parity(dtype, rows, k):
     td = torch.float64 if dtype == np.float64 else torch.float32
     alpha = workloads.cfg4_params(rows, k, seed=3, dtype=td)
