@@ -1,6 +1,6 @@
 """Time build variants of libbrng (tools/variants/*.so) on one kernel.
 
-usage: python tools/variant_time.py gibbs|gibbs1|gamma|gamma32|dirichlet|gaussian|uniform [lib ...]
+usage: python tools/variant_time.py gibbs|gibbs1|gamma|gamma32|dirichlet|gaussian|uniform|exponential [lib ...]
 Each variant runs in its own process (BRNG_LIB=...); prints ms and a hash of
 the outputs so variants can be checked for identical results.
 """
@@ -59,6 +59,15 @@ elif what == "gamma":
     def run():
         B.brng_set_offset(h, 0)
         B.brng_gamma_f64(h, p["alpha"], p["beta"], o, n, None)
+    outs = [o]
+elif what == "exponential":
+    n = 1 << 28
+    lam = W.exp_params(n, seed=7, device=dev)
+    o = torch.empty(n, device=dev)
+    h = B.brng_create(7, 5); B.brng_set_cuda_stream(h, s)
+    def run():
+        B.brng_set_offset(h, 0)
+        B.brng_exponential_f32(h, lam, o, n)
     outs = [o]
 elif what in ("gaussian", "uniform"):
     n = 1 << 28
