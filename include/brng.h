@@ -102,7 +102,9 @@ BRNG_API int brng_create(uint64_t seed, uint64_t stream_id, brng_t* out);
 /* Synchronise the handle's stream and free the handle and its scratch. */
 BRNG_API int brng_destroy(brng_t h);
 /* Enqueue subsequent calls on this cudaStream_t (e.g. torch's current stream;
- * NULL = legacy default stream).  Not owned by the handle. */
+ * NULL = legacy default stream).  Not owned by the handle.  Switching streams
+ * makes the new stream wait for the work already enqueued on the old one
+ * (the handle's device scratch is shared by its calls). */
 BRNG_API int brng_set_cuda_stream(brng_t h, void* cuda_stream);
 BRNG_API int brng_get_offset(brng_t h, uint64_t* block_cursor);
 /* Reposition the cursor (resume a checkpoint, or shard: rank r of a data-

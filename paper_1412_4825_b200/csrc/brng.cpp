@@ -49,6 +49,7 @@ struct brng_handle_s {
   double* d_partials;          // Gibbs per-CTA partials
   size_t partials_cap;         // in doubles
   double* d_totals;            // Gibbs totals scratch for host `totals` pointers
+  cudaEvent_t ev_switch;       // orders work across brng_set_cuda_stream
   // host-staging pipeline (created on the first host-pointer call)
   cudaStream_t s_in, s_out;
   cudaEvent_t ev_in[kSlots], ev_k[kSlots], ev_out[kSlots];
@@ -410,6 +411,11 @@ int brng_create(uint64_t seed, uint64_t stream_id, brng_t* out) {
     delete h;
     return BRNG_ERR_CUDA;
   }
+  if (cudaEventCreateWithFlags(&h->ev_switch, cudaEventDisableTiming) != cudaSuccess) {
+    cudaFree(h->d_err);
+    delete h;
+    return BRNG_ERR_CUDA;
+  }
   *out = h;
   return BRNG_OK;
 }
@@ -419,6 +425,7 @@ int brng_destroy(brng_t h) {
   DeviceGuard dg(h);
   cudaStreamSynchronize(h->stream);
   cudaFree(h->d_err);
+  cudaEventDestroy(h->ev_switch);
   if (h->d_partials) cudaFree(h->d_partials);
   if (h->d_totals) cudaFree(h->d_totals);
   if (h->pipe_ready) {
@@ -439,7 +446,18 @@ int brng_destroy(brng_t h) {
 
 int brng_set_cuda_stream(brng_t h, void* s) {
   if (!h) return BRNG_ERR_NULL;
-  h->stream = static_cast<cudaStream_t>(s);
+  cudaStream_t ns = static_cast<cudaStream_t>(s);
+  if (ns != h->stream) {
+    // The handle's device scratch (work counter, Gibbs partials) is reused by
+    // every call: work already enqueued on the old stream must finish before
+    // the new stream's calls touch it.
+    DeviceGuard dg(h);
+    if (dg.status()) return dg.status();
+    cudaError_t e = cudaEventRecord(h->ev_switch, h->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ns, h->ev_switch, 0);
+    if (e != cudaSuccess) return BRNG_ERR_CUDA;
+    h->stream = ns;
+  }
   return BRNG_OK;
 }
 int brng_get_offset(brng_t h, uint64_t* c) {

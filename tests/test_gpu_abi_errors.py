@@ -51,3 +51,31 @@ def test_handles_are_independent_and_keyed():
             B.brng_std_uniform_f64(h, out, n)
         assert not torch.equal(o[0], o[1]) and not torch.equal(o[0], o[2])
         assert B.brng_get_key(h2) == (5, 1)
+
+
+def test_stream_switch_orders_the_handles_work():
+    """A handle's calls share device scratch (the Gamma/Dirichlet work
+    counter, the Gibbs partials): after brng_set_cuda_stream the new stream
+    waits for the old one, so back-to-back calls on two streams give the
+    results of the same calls on one stream."""
+    import workloads
+    n = 1 << 25                  # ~0.4 ms kernels: the second call is enqueued mid-run
+    p = workloads.cfg3_params(n, seed=11, device=dev())
+    ref = [torch.empty(n, dtype=torch.float64, device=dev()) for _ in range(2)]
+    got = [torch.empty(n, dtype=torch.float64, device=dev()) for _ in range(2)]
+    with handle(11, 0) as h:
+        for o in ref:
+            B.brng_gamma_f64(h, p["alpha"], p["beta"], o, n)
+        torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    h = B.brng_create(11, 0)
+    try:
+        B.brng_set_cuda_stream(h, s1.cuda_stream)
+        B.brng_gamma_f64(h, p["alpha"], p["beta"], got[0], n)
+        B.brng_set_cuda_stream(h, s2.cuda_stream)
+        B.brng_gamma_f64(h, p["alpha"], p["beta"], got[1], n)
+        torch.cuda.synchronize()
+        assert B.brng_device_errors(h) == 0
+    finally:
+        B.brng_destroy(h)
+    assert torch.equal(got[0], ref[0]) and torch.equal(got[1], ref[1])
