@@ -522,10 +522,21 @@ def e2e_run(wl, torch, B, args, allreduce, world, dist):
         B.brng_set_cuda_stream(h, s_b.cuda_stream)
 
     def step_concurrent():
-        ta = threading.Thread(target=group_gibbs)
+        err = []
+
+        def run_gibbs():
+            try:
+                group_gibbs()
+            except BaseException as e:          # re-raised below: no silent e2e number
+                err.append(e)
+        ta = threading.Thread(target=run_gibbs)
         ta.start()
-        group_io()
-        ta.join()
+        try:
+            group_io()
+        finally:
+            ta.join()
+        if err:
+            raise err[0]
         reduce()
 
     def step_serial():
