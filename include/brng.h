@@ -13,9 +13,10 @@
  *  Handle.   A brng_t is the GPU recast of the paper's BatchRNG object
  *            (P:L54-66): the engine state is (seed, stream_id, block cursor)
  *            instead of VSL stream state + buffers + buffer counters.  It also
- *            owns a few bytes of device scratch (an invalid-sample counter and
- *            Gibbs reduction partials).  One handle = one consumer at a time;
- *            distinct handles may be used concurrently on distinct streams.
+ *            owns a little device scratch (an invalid-sample counter, the
+ *            Gamma/Dirichlet work counter, Gibbs reduction partials) shared
+ *            by its calls.  One handle = one consumer at a time; distinct
+ *            handles may be used concurrently on distinct streams.
  *  Counter map (R-01, R-02).  Every random word is a word of a Philox4x32-10
  *            block with key = (lo32 seed, hi32 seed) and counter = (lo32 pos,
  *            hi32 pos, lo32 stream, hi32 stream); pos is a 64-bit BLOCK index.
@@ -86,7 +87,7 @@ typedef enum brng_status {
     BRNG_ERR_CUDA = -3,      /* CUDA runtime error (launch, copy, alloc)   */
     BRNG_ERR_PARAM = -4,     /* invalid scalar argument                    */
     BRNG_ERR_OVERFLOW = -5,  /* cursor + span would pass 2^64              */
-    BRNG_ERR_STATE = -6      /* handle used on a different device          */
+    BRNG_ERR_STATE = -6      /* the handle's device cannot be made current */
 } brng_status;
 
 /* ---- lifecycle (the paper's constructor / destructor) ---------- */
@@ -96,8 +97,8 @@ typedef enum brng_status {
  * calling thread, and leaves the caller's current device unchanged.
  * seed: Philox key (any value, including 0).  stream_id: Philox stream (upper
  * counter half) used by every fill/Gamma/Dirichlet call; Gibbs chain c uses
- * stream stream_id + c.  *out receives the handle.  Allocates ~4 KB device
- * scratch. */
+ * stream stream_id + c.  *out receives the handle.  Allocates 16 B of device
+ * counters (the Gibbs partials, ~0.6 MB, on the first Gibbs call). */
 BRNG_API int brng_create(uint64_t seed, uint64_t stream_id, brng_t* out);
 /* Synchronise the handle's stream and free the handle and its scratch. */
 BRNG_API int brng_destroy(brng_t h);
