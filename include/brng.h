@@ -98,7 +98,9 @@ typedef enum brng_status {
  * seed: Philox key (any value, including 0).  stream_id: Philox stream (upper
  * counter half) used by every fill/Gamma/Dirichlet call; Gibbs chain c uses
  * stream stream_id + c.  *out receives the handle.  Allocates 16 B of device
- * counters (the Gibbs partials, ~0.6 MB, on the first Gibbs call). */
+ * counters (the Gibbs partials, ~0.6 MB, on the first Gibbs call; a binary32
+ * Dirichlet call with K > 1024 grows a scratch of one row of K doubles per
+ * resident warp, at most 2 GB). */
 BRNG_API int brng_create(uint64_t seed, uint64_t stream_id, brng_t* out);
 /* Synchronise the handle's stream and free the handle and its scratch. */
 BRNG_API int brng_destroy(brng_t h);

@@ -49,6 +49,8 @@ struct brng_handle_s {
   double* d_partials;          // Gibbs per-CTA partials
   size_t partials_cap;         // in doubles
   double* d_totals;            // Gibbs totals scratch for host `totals` pointers
+  double* d_dir_scratch;       // binary32 large-K Dirichlet rows (grown on demand)
+  size_t dir_scratch_cap;      // in doubles
   cudaEvent_t ev_switch;       // orders work across brng_set_cuda_stream
   // host-staging pipeline (created on the first host-pointer call)
   cudaStream_t s_in, s_out;
@@ -364,7 +366,28 @@ int dirichlet_common(brng_t h, int dtype, const void* alpha, uint64_t n_rows, ui
   uint64_t base;
   if ((st = reserve(h, n, 1, BRNG_GAMMA_STRIDE, &base))) return st;
   std::vector<Arr> arrs = {{alpha, esize * k, false}, {out, esize * k, true}, {trials, k, true}};
-  const Ctx ctx = make_ctx(h);
+  Ctx ctx = make_ctx(h);
+  // binary32 rows too long for shared memory park their Gammas in a
+  // handle-owned scratch (one row per resident warp) instead of recomputing
+  // them; above 2 GB of scratch the kernel recomputes
+  const size_t scr = brng::dirichlet_scratch_len(dtype, k, ctx);
+  if (scr && scr <= (size_t(1) << 28)) {
+    if (scr > h->dir_scratch_cap) {
+      if (h->d_dir_scratch) {
+        cudaStreamSynchronize(h->stream);
+        cudaFree(h->d_dir_scratch);
+        h->d_dir_scratch = nullptr;
+        h->dir_scratch_cap = 0;
+      }
+      if (cudaMalloc(&h->d_dir_scratch, scr * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        h->d_dir_scratch = nullptr;       // fall back to recomputing the rows
+      } else {
+        h->dir_scratch_cap = scr;
+      }
+    }
+    ctx.dir_scratch = h->d_dir_scratch;
+  }
   st = run(h, arrs, n_rows, 1, [&](uint64_t r0, uint64_t nr, const std::vector<void*>& d, bool) {
     return brng::launch_dirichlet(dtype, d[0], nr, k, d[1], static_cast<uint8_t*>(d[2]),
                                   base + (uint64_t)BRNG_GAMMA_STRIDE * r0 * k, ctx);
@@ -405,6 +428,7 @@ int brng_create(uint64_t seed, uint64_t stream_id, brng_t* out) {
   h->seed = seed; h->stream_id = stream_id; h->cursor = 0;
   h->device = dev; h->num_sms = sms; h->stream = nullptr;
   h->d_partials = nullptr; h->partials_cap = 0; h->d_totals = nullptr;
+  h->d_dir_scratch = nullptr; h->dir_scratch_cap = 0;
   h->pipe_ready = false; h->stage_cap = 0;
   if (cudaMalloc(&h->d_err, 2 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMemset(h->d_err, 0, 2 * sizeof(unsigned long long)) != cudaSuccess) {
@@ -428,6 +452,7 @@ int brng_destroy(brng_t h) {
   cudaEventDestroy(h->ev_switch);
   if (h->d_partials) cudaFree(h->d_partials);
   if (h->d_totals) cudaFree(h->d_totals);
+  if (h->d_dir_scratch) cudaFree(h->d_dir_scratch);
   if (h->pipe_ready) {
     cudaStreamSynchronize(h->s_in);
     cudaStreamSynchronize(h->s_out);

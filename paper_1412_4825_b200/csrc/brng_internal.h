@@ -19,6 +19,7 @@ struct Ctx {
   uint64_t stream_id;        // Philox stream of fills / Gamma / Dirichlet
   unsigned long long* err;   // device invalid-sample counter
   unsigned long long* work;  // device work counter (dynamic chunk assignment)
+  double* dir_scratch = nullptr;   // binary32 large-K Dirichlet: one row of Gammas per warp
 };
 
 // K1/K2: raw words, standard uniforms and per-sample-parameter transforms.
@@ -31,6 +32,9 @@ cudaError_t launch_fill(int dist, int dtype, const void* p0, const void* p1, voi
 cudaError_t launch_gamma(int dtype, const void* alpha, const void* beta, void* out,
                          uint8_t* trials, uint64_t n, uint64_t base, const Ctx& ctx);
 // K4: Dirichlet rows (Gamma + warp-shuffle normalisation).
+// Doubles of scratch the binary32 large-K Dirichlet launch uses (0: none,
+// the rows are recomputed instead): one row of K Gammas per resident warp.
+size_t dirichlet_scratch_len(int dtype, uint64_t k, const Ctx& ctx);
 cudaError_t launch_dirichlet(int dtype, const void* alpha, uint64_t n_rows, uint64_t k,
                              void* out, uint8_t* trials, uint64_t base, const Ctx& ctx);
 // K5-K7: Gibbs chains + stats + histogram, then the fixed-order reduction.

@@ -218,13 +218,17 @@ struct DirArgs {
   unsigned long long* err;
   uint32_t rpw;          // rows per warp queue (smem kernel)
   unsigned long long* work;   // dynamic group counter (BRNG_GAMMA_DYN)
+  double* scratch;            // two-pass binary32: [gridDim.x * 4][k] Gammas (or null)
 };
 
 constexpr int kDirThreads = 128;     // 4 warps / CTA, one row per warp
 #ifndef BRNG_DIR_SMEM_K
 #define BRNG_DIR_SMEM_K 2048
 #endif
-constexpr uint64_t kDirSmemK = BRNG_DIR_SMEM_K;   // rows up to this K are staged in smem
+constexpr uint64_t kDirSmemK = BRNG_DIR_SMEM_K;
+#ifndef BRNG_DIR_SMEM_K32
+#define BRNG_DIR_SMEM_K32 1024     // binary32 rows up to this K use shared memory
+#endif   // rows up to this K are staged in smem
 #ifndef BRNG_DIR_TARGET
 #define BRNG_DIR_TARGET 512
 #endif
@@ -306,14 +310,38 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(const __gr
   const uint64_t warp = ((uint64_t)blockIdx.x * kDirThreads + threadIdx.x) >> 5;
   const uint64_t n_warps = ((uint64_t)gridDim.x * kDirThreads) >> 5;
   uint32_t nbad = 0, nbad2 = 0;
-  for (uint64_t row = warp; row < a.n_rows; row += n_warps) {
+  // with scratch (one resident wave) warps take rows from the work counter;
+  // otherwise a static grid-stride assignment
+  auto fetch = [&]() -> uint64_t {
+    unsigned long long r = 0;
+    if ((threadIdx.x & 31) == 0) r = atomicAdd(a.work, 1ull);
+    return __shfl_sync(kFull, r, 0);
+  };
+  for (uint64_t row = a.scratch ? fetch() : warp; row < a.n_rows;
+       row = a.scratch ? fetch() : row + n_warps) {
     const uint64_t beg = row * a.k;
     auto load = [&](uint64_t i, double& al, double& be) {
       al = (double)__ldg(a.alpha + i);
       be = 1.0;
     };
     double s = 0.0;
-    if constexpr (sizeof(T) == 8) {
+    if (sizeof(T) == 4 && a.scratch) {
+      // binary32 with scratch: the warp's own row of binary64 Gammas
+      double* g_row = a.scratch + warp * a.k;
+      mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
+               [&](uint64_t i, double v, uint32_t t) {
+                 s += v;
+                 g_row[i - beg] = v;
+                 if (a.trials) a.trials[i] = (uint8_t)t;
+               },
+               nbad, q);
+      s = warp_sum(s);
+      const double inv = 1.0 / s;
+      __syncwarp();
+      const uint32_t lane = threadIdx.x & 31;
+      for (uint64_t j = lane; j < a.k; j += 32) a.out[beg + j] = (T)(g_row[j] * inv);
+      __syncwarp();
+    } else if constexpr (sizeof(T) == 8) {
       mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
                [&](uint64_t i, double v, uint32_t t) {
                  s += v;
@@ -365,16 +393,31 @@ cudaError_t gamma_typed(const T* alpha, const T* beta, T* out, uint8_t* trials, 
   return cudaGetLastError();
 }
 
+int dir2_ctas_per_sm() {
+  static int cached = [] {
+    int v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, dirichlet_2pass_kernel<float>,
+                                                      kDirThreads, 0) != cudaSuccess ||
+        v < 1)
+      v = 1;
+    return v;
+  }();
+  return cached;
+}
+
 template <typename T>
 cudaError_t dirichlet_typed(const T* alpha, uint64_t n_rows, uint64_t k, T* out,
                             uint8_t* trials, uint64_t base, const Ctx& ctx) {
   DirArgs<T> a{alpha, out, trials, n_rows, k, base, ctx.stream_id,
-                 make_round_keys(ctx.k0, ctx.k1, ctx.stream_id), ctx.err, 1u, ctx.work};
+                 make_round_keys(ctx.k0, ctx.k1, ctx.stream_id), ctx.err, 1u, ctx.work,
+                 nullptr};
   const uint64_t ctas_needed = (n_rows + 3) / 4;
   // binary64 output parks the row's Gammas in the output row instead (no
   // shared-memory occupancy cost): faster from K = 1024 on (tools/dirichlet_k.py:
   // 2^27 components, K = 1024: 2.38 -> 2.12 ms, K = 2048: 3.71 -> 2.10 ms)
-  const uint64_t smem_k = sizeof(T) == 8 ? (kDirSmemK < 512 ? kDirSmemK : 512) : kDirSmemK;
+  const uint64_t smem_k = sizeof(T) == 8 ? (kDirSmemK < 512 ? kDirSmemK : 512)
+                                         : (kDirSmemK < BRNG_DIR_SMEM_K32 ? kDirSmemK
+                                                                          : BRNG_DIR_SMEM_K32);
   if (k <= smem_k) {
     const uint64_t r = kDirTarget / k;
     a.rpw = (uint32_t)(r < 1 ? 1 : (r > 8 ? 8 : r));
@@ -403,7 +446,14 @@ cudaError_t dirichlet_typed(const T* alpha, uint64_t n_rows, uint64_t k, T* out,
     const unsigned g = (unsigned)(ctas < cap ? ctas : cap);
     dirichlet_smem_kernel<T><<<g, kDirThreads, smem, ctx.stream>>>(a);
   } else {
-    const uint64_t cap = (uint64_t)ctx.num_sms * 16 * 8;
+    uint64_t cap = (uint64_t)ctx.num_sms * 16 * 8;
+    if (sizeof(T) == 4 && ctx.dir_scratch) {
+      // one resident wave; warp w parks its rows' Gammas in scratch row w
+      a.scratch = ctx.dir_scratch;
+      cap = (uint64_t)ctx.num_sms * dir2_ctas_per_sm();
+      cudaError_t e0 = cudaMemsetAsync(ctx.work, 0, sizeof(unsigned long long), ctx.stream);
+      if (e0 != cudaSuccess) return e0;
+    }
     const unsigned g = (unsigned)(ctas_needed < cap ? ctas_needed : cap);
     dirichlet_2pass_kernel<T><<<g, kDirThreads, 0, ctx.stream>>>(a);
   }
@@ -420,6 +470,12 @@ cudaError_t launch_gamma(int dtype, const void* alpha, const void* beta, void* o
   return gamma_typed<double>(static_cast<const double*>(alpha),
                              static_cast<const double*>(beta), static_cast<double*>(out), trials,
                              n, base, ctx);
+}
+
+size_t dirichlet_scratch_len(int dtype, uint64_t k, const Ctx& ctx) {
+  if (dtype != kF32 || k <= (kDirSmemK < BRNG_DIR_SMEM_K32 ? kDirSmemK : BRNG_DIR_SMEM_K32))
+    return 0;
+  return (size_t)ctx.num_sms * dir2_ctas_per_sm() * (kDirThreads / 32) * k;
 }
 
 cudaError_t launch_dirichlet(int dtype, const void* alpha, uint64_t n_rows, uint64_t k,

@@ -204,6 +204,18 @@ def test_host_pipeline_multi_chunk_gamma_dirichlet():
         xd = torch.empty(D, K, device=dev())
         B.brng_dirichlet_f32(h, al.to(dev()), D, K, xd, None)
     assert np.array_equal(xh, xd.cpu().numpy())
+    # long rows (the scratch / in-place paths), both output types, 2+ chunks
+    for dt, npt, fn in ((torch.float32, np.float32, B.brng_dirichlet_f32),
+                        (torch.float64, np.float64, B.brng_dirichlet_f64)):
+        D, K = 9_001, 3_000
+        al = workloads.cfg4_params(D, K, seed=23, dtype=dt)
+        xh = np.empty((D, K), npt)
+        with handle(23) as h:
+            fn(h, al.numpy(), D, K, xh, None)
+        with handle(23) as h:
+            xd = torch.empty(D, K, dtype=dt, device=dev())
+            fn(h, al.to(dev()), D, K, xd, None)
+        assert np.array_equal(xh, xd.cpu().numpy()), dt
 
 
 @pytest.mark.slow
