@@ -33,14 +33,14 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None,
-          defines: tuple = ()) -> str:
+          defines: tuple = (), tag: str = "") -> str:
     """Compile libbrng.so (or `out`, with extra -D `defines`, for experiments)."""
     lib = out or LIB
     if out is None and not force and not _stale():
         return LIB
     objs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src + ".o")
+        obj = os.path.join(CSRC, src + (f".{tag}" if tag else "") + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I",
                os.path.join(ROOT, "include"), "-c",
                "-x", "cu", os.path.join(CSRC, src), "-o", obj]

@@ -152,6 +152,143 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
   if (qn) drain(qn);
 }
 
+// ---- lockstep schedule (BRNG_LOCKSTEP) ---------------------------------------
+// Iteration k of a warp runs trial 1 of samples beg + 32k + lane in lock step:
+// the parameter loads are coalesced and issued one iteration ahead (the next
+// samples are known), the stores are coalesced, and the only per-iteration
+// bookkeeping is two ballots.  The rare rejected samples (cfg3 1.7%, cfg4 4.2%
+// of samples) are parked with their next trial index in a per-warp retry list
+// and rerun 32 at a time.  Accepted alpha<1 samples are boosted in place when
+// most lanes need it (cfg4: 91% of components) and parked in the boost queue
+// otherwise (cfg3: 36%), so the boost runs as a (nearly) full warp either way.
+// Values are pure functions of (counters, parameters), as for mt_queue.
+// Measured (tools/variant_time.py, identical output hashes): cfg3 0.853 ms
+// (queue) vs 0.912-0.936 (lockstep), cfg4 4.331 vs 4.343-4.346: the lockstep
+// loop carries ~28 constant-bank reloads (LDC/LDCU) per iteration that the
+// queue loop hoists, eating the bookkeeping it saves.  Kept as a build option;
+// the queue is the default.
+#ifndef BRNG_LOCKSTEP
+#define BRNG_LOCKSTEP 0
+#endif
+#ifndef BRNG_INPLACE_MIN
+#define BRNG_INPLACE_MIN 22
+#endif
+constexpr int kRetryCap = 64;
+
+template <typename P, typename Load, typename Sink>
+__device__ __forceinline__ void mt_lockstep(uint64_t beg, uint64_t end, uint64_t base,
+                                            const RoundKeys& rk, const Tables& tb, Load load,
+                                            Sink sink, uint32_t& nbad, BoostItem* q,
+                                            uint64_t* rq) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  uint32_t qn = 0, rn = 0;                           // warp-uniform queue lengths
+  // lanes [0, n) take the last n boost-queue entries, boost and sink them
+  auto drain = [&](uint32_t n) {
+    __syncwarp();
+    if (lane < n) {
+      const BoostItem it = q[qn - n + lane];
+      const uint64_t ii = it.i_t & 0x00FFFFFFFFFFFFFFull;
+      P qa, qb;
+      load(ii, qa, qb);
+      const uint4 wb = philox_block_rk(base + (uint64_t)kStride * ii, rk);
+      sink(ii, mt_boost(wb, it.g, (double)qa, tb) * (double)qb, (uint32_t)(it.i_t >> 56));
+    }
+    qn -= n;
+    __syncwarp();
+  };
+  // lanes [0, n) take the last n retry entries (sample | next trial << 56)
+  // and run their trials until acceptance; boosts in place (rare here)
+  auto retry_pass = [&](uint32_t n) {
+    __syncwarp();
+    const bool act = lane < n;
+    uint64_t e = 0;
+    if (act) e = rq[rn - n + lane];
+    __syncwarp();
+    rn -= n;
+    const uint64_t ii = e & 0x00FFFFFFFFFFFFFFull;
+    uint32_t tt = (uint32_t)(e >> 56);
+    P alr = P(1), ber = P(1);
+    if (act) load(ii, alr, ber);
+    const double al = (double)alr, be = (double)ber;
+    double g = 0.0;
+    bool fin = !act, ok = false;
+    while (__any_sync(kFull, !fin)) {
+      if (!fin) {
+        double d;
+        const uint4 w = philox_block_rk(base + (uint64_t)kStride * ii + tt, rk);
+        if (mt_trial(w, al, d, g, tb)) {
+          fin = true; ok = true;
+        } else if (++tt > kMaxTrial) {
+          fin = true;
+        }
+      }
+    }
+    if (act) {
+      if (!ok) {
+        ++nbad;
+        sink(ii, qnan(), 0u);
+      } else {
+        double v = g;
+        if (al < 1.0) v = mt_boost(philox_block_rk(base + (uint64_t)kStride * ii, rk), g, al, tb);
+        sink(ii, v * be, tt);
+      }
+    }
+  };
+  // parameters of the next iteration, kept in their storage type (converting
+  // at the load would wait for it)
+  P a_nx = P(1), b_nx = P(1);
+  if (beg + lane < end) load(beg + lane, a_nx, b_nx);
+  uint64_t pos = base + (uint64_t)kStride * (beg + lane) + 1;   // trial-1 block of sample i
+  for (uint64_t i0 = beg; i0 < end; i0 += 32, pos += 32ull * kStride) {
+    const uint64_t i = i0 + lane;
+    const double alpha = (double)a_nx, beta = (double)b_nx;
+    if (i + 32 < end) load(i + 32, a_nx, b_nx);
+    bool boost = false, retry = false;
+    double g = 0.0;
+    if (i < end) {
+      const uint4 w = philox_block_rk(pos, rk);
+      const bool valid = isfinite(alpha) && isfinite(beta) && alpha > 0.0 && beta > 0.0;
+      double d;
+      const bool acc = mt_trial(w, alpha, d, g, tb);
+      if (!valid) {
+        ++nbad;
+        sink(i, qnan(), 0u);
+      } else if (!acc) {
+        retry = true;
+      } else if (alpha < 1.0) {
+        boost = true;
+      } else {
+        sink(i, g * beta, 1u);
+      }
+    }
+    const uint32_t rm = __ballot_sync(kFull, retry);
+    if (rm) {
+      if (retry) rq[rn + __popc(rm & lt)] = i | (2ull << 56);
+      rn += __popc(rm);
+    }
+    const uint32_t bm = __ballot_sync(kFull, boost);
+    if (__popc(bm) >= BRNG_INPLACE_MIN) {
+      if (boost) sink(i, mt_boost(philox_block_rk(pos - 1, rk), g, alpha, tb) * beta, 1u);
+    } else if (bm) {
+      if (boost) {
+        BoostItem it;
+        it.g = g;
+#if !BRNG_SLIM_QUEUE
+        it.alpha = alpha; it.beta = beta;
+#endif
+        it.i_t = i | (1ull << 56);
+        q[qn + __popc(bm & lt)] = it;
+      }
+      qn += __popc(bm);
+      if (qn >= 32) drain(32);
+    }
+    if (rn >= 32) retry_pass(32);
+  }
+  while (rn) retry_pass(rn < 32 ? rn : 32);
+  if (qn) drain(qn);
+}
+
 template <typename T>
 struct GammaArgs {
   const T* alpha;
@@ -176,6 +313,10 @@ template <typename T>
 #endif
 __global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(const __grid_constant__ GammaArgs<T> a) {
   __shared__ BoostItem qs[kThreads / 32][kBoostCap];
+#if BRNG_LOCKSTEP
+  __shared__ uint64_t rqs[kThreads / 32][kRetryCap];
+  uint64_t* rq = rqs[threadIdx.x >> 5];
+#endif
   const Tables tb{};
   BoostItem* q = qs[threadIdx.x >> 5];
   const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -193,17 +334,30 @@ __global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(const 
   for (uint64_t beg = warp * kChunk; beg < a.n; beg += n_warps * kChunk) {
 #endif
     const uint64_t end = beg + kChunk < a.n ? beg + kChunk : a.n;
+#if BRNG_LOCKSTEP
+    mt_lockstep<T>(
+        beg, end, a.base, a.rk, tb,
+        [&](uint64_t i, T& al, T& be) {
+          al = __ldg(a.alpha + i);
+          be = __ldg(a.beta + i);
+        },
+#else
     mt_queue(
         beg, end, a.base, a.rk, tb,
         [&](uint64_t i, double& al, double& be) {
           al = (double)__ldg(a.alpha + i);
           be = (double)__ldg(a.beta + i);
         },
+#endif
         [&](uint64_t i, double v, uint32_t t) {
           a.out[i] = (T)v;
           if (a.trials) a.trials[i] = (uint8_t)t;
         },
+#if BRNG_LOCKSTEP
+        nbad, q, rq);
+#else
         nbad, q);
+#endif
   }
   flush_errors(a.err, nbad);
 }
@@ -247,6 +401,10 @@ template <typename T>
 __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __grid_constant__ DirArgs<T> a) {
   extern __shared__ double gsm[];
   __shared__ BoostItem qs[kDirThreads / 32][kBoostCap];
+#if BRNG_LOCKSTEP
+  __shared__ uint64_t rqs[kDirThreads / 32][kRetryCap];
+  uint64_t* rq = rqs[threadIdx.x >> 5];
+#endif
   const Tables tb{};
   BoostItem* q = qs[threadIdx.x >> 5];
   const uint32_t lane = threadIdx.x & 31;
@@ -271,17 +429,30 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __gri
     const uint64_t row0 = grp * a.rpw;
     const uint64_t rows = a.n_rows - row0 < a.rpw ? a.n_rows - row0 : a.rpw;
     const uint64_t beg = row0 * a.k;
+#if BRNG_LOCKSTEP
+    mt_lockstep<T>(
+        beg, beg + rows * a.k, a.base, a.rk, tb,
+        [&](uint64_t i, T& al, T& be) {
+          al = __ldg(a.alpha + i);
+          be = T(1);
+        },
+#else
     mt_queue(
         beg, beg + rows * a.k, a.base, a.rk, tb,
         [&](uint64_t i, double& al, double& be) {
           al = (double)__ldg(a.alpha + i);
           be = 1.0;
         },
+#endif
         [&](uint64_t i, double v, uint32_t t) {
           g_grp[i - beg] = v;
           if (a.trials) a.trials[i] = (uint8_t)t;
         },
+#if BRNG_LOCKSTEP
+        nbad, q, rq);
+#else
         nbad, q);
+#endif
     __syncwarp();
     for (uint64_t r = 0; r < rows; ++r) {
       const double* g_row = g_grp + r * a.k;

@@ -127,6 +127,46 @@ def gamma_compare(got, trials, alpha, beta, seed, stream, base, i0=0, dtype=np.f
     return _decide(got, trials, ref, tref, alpha, seed, stream, base, idx, dtype)
 
 
+def value_check(got, ref, scale, dtype, cond_at=None, what="values"):
+    """The value criterion with its relaxations made auditable.
+
+    Bound = tau * scale * cond + EPS_MIN, where cond = cond_at(k) (the
+    Marsaglia-Tsang condition number, Gamma/Dirichlet) is applied only where
+    the plain bound tau * scale + EPS_MIN fails.  Returns dict(ratio = max
+    error / bound (must be <= 1), n = values compared, worst_plain_rel = max
+    |x - x_ref| / |x_ref| over x_ref != 0, n_plain_fail = samples outside the
+    literal SURVEY 8c.5 bound tau |x_ref| + one subnormal, n_floor = those
+    rescued by the tau * smallest-normal floor alone, n_cond = those that
+    needed the condition factor)."""
+    dtype = np.dtype(dtype)
+    got = _np(got).astype(np.float64)
+    ref = np.asarray(ref).astype(np.float64)
+    scale = np.array(scale, dtype=np.float64, copy=True)
+    nan_g, nan_r = np.isnan(got), np.isnan(ref)
+    assert np.array_equal(nan_g, nan_r), f"{what}: NaN pattern differs"
+    m = ~nan_r
+    got, ref, scale = got[m], ref[m], scale[m]
+    err = np.abs(got - ref)
+    tau, sub = TAU[dtype], float(np.finfo(dtype).smallest_subnormal)
+    nz = ref != 0
+    worst_plain = float(np.max(err[nz] / np.abs(ref[nz]))) if nz.any() else 0.0
+    plain_fail = ~(err <= tau * np.abs(ref) + sub)
+    loose = ~(err <= tau * scale + EPS_MIN[dtype])
+    n_floor = int(np.count_nonzero(plain_fail & ~loose & (err <= tau * np.abs(ref) + EPS_MIN[dtype])))
+    if cond_at is not None:
+        ks = np.flatnonzero(m)
+        for k in np.flatnonzero(loose):
+            scale[k] *= max(1.0, cond_at(int(ks[k])))
+    bound = tau * scale + EPS_MIN[dtype]
+    ratio = float(np.max(err / bound)) if err.size else 0.0
+    if ratio > 1.0:
+        k = int(np.argmax(err / bound))
+        raise AssertionError(f"{what}: error ratio {ratio:.3g}: got {got[k]!r} ref {ref[k]!r}")
+    return dict(ratio=ratio, n=int(err.size), worst_plain_rel=worst_plain,
+                n_plain_fail=int(np.count_nonzero(plain_fail)), n_floor=n_floor,
+                n_cond=int(np.count_nonzero(loose)))
+
+
 def _decide(got, trials, ref, tref, alpha, seed, stream, base, idx, dtype):
     same = trials == tref
     n_tie = n_fail = 0
@@ -141,19 +181,15 @@ def _decide(got, trials, ref, tref, alpha, seed, stream, base, idx, dtype):
             n_tie += 1
         else:
             n_fail += 1; fails.append(int(idx[k]))
-    scale = np.abs(ref.astype(np.float64))
     # conditioning: g = d (1 + c z)^3 has condition 3|c z / (1 + c z)| in z, so
     # any 1-ulp difference in z (log, sqrt, cos) is amplified near 1 + cz -> 0;
-    # the scale carries that factor
-    g64, r64 = got.astype(np.float64), ref.astype(np.float64)
-    with np.errstate(invalid="ignore"):
-        loose = same & ~(np.abs(g64 - r64) <= TAU[dtype] * scale + EPS_MIN[dtype])
-    for k in np.flatnonzero(loose):
-        scale[k] *= max(1.0, gamma_condition(seed, stream, base, int(idx[k]), float(alpha[k]),
-                                             int(tref[k])))
-    ratio = check_close(got[same], ref[same], scale[same], dtype,
-                        "gamma values") if same.any() else 0.0
-    return dict(n=len(got), n_tie=n_tie, n_fail=n_fail, ratio=ratio, fails=fails[:10])
+    # the scale carries that factor where the plain bound fails
+    ks = np.flatnonzero(same)
+    vc = value_check(got[same], ref[same], np.abs(ref[same].astype(np.float64)), dtype,
+                     lambda j: gamma_condition(seed, stream, base, int(idx[ks[j]]),
+                                               float(alpha[ks[j]]), int(tref[ks[j]])),
+                     "gamma values") if same.any() else dict(ratio=0.0)
+    return dict(n=len(got), n_tie=n_tie, n_fail=n_fail, fails=fails[:10], **vc)
 
 
 def gamma_condition(seed, stream, base, i, alpha, t):
@@ -185,18 +221,15 @@ def dirichlet_compare(got, trials, alpha, seed, stream, base, row0=0, dtype=np.f
         else:
             n_fail += 1
     ok = ~tie_rows
-    scale = np.abs(ref.astype(np.float64))
-    with np.errstate(invalid="ignore"):
-        loose = ok[:, None] & ~(np.abs(got.astype(np.float64) - ref) <= TAU[dtype] * scale +
-                                EPS_MIN[dtype])
-    for r, c in zip(*np.nonzero(loose)):
-        # x_k = g_k / S: the row sum is well conditioned; g_k carries its own
-        # Marsaglia-Tsang conditioning (see gamma_compare)
-        scale[r, c] *= max(1.0, gamma_condition(seed, stream, base, (row0 + r) * k + c,
-                                                float(alpha[r, c]), int(tref[r, c])))
-    ratio = check_close(got[ok].reshape(-1), ref[ok].reshape(-1), scale[ok].reshape(-1), dtype,
-                        "dirichlet")
-    return dict(n=got.size, n_tie=n_tie, n_fail=n_fail, ratio=ratio)
+    rr, cc = np.nonzero(np.broadcast_to(ok[:, None], got.shape))
+    # x_k = g_k / S: the row sum is well conditioned; g_k carries its own
+    # Marsaglia-Tsang conditioning (see gamma_compare)
+    vc = value_check(got[ok].reshape(-1), ref[ok].reshape(-1),
+                     np.abs(ref[ok].reshape(-1).astype(np.float64)), dtype,
+                     lambda j: gamma_condition(seed, stream, base, (row0 + int(rr[j])) * k + int(cc[j]),
+                                               float(alpha[rr[j], cc[j]]), int(tref[rr[j], cc[j]])),
+                     "dirichlet")
+    return dict(n=got.size, n_tie=n_tie, n_fail=n_fail, **vc)
 
 
 def windows(n, n_windows=32, width=256, seed=0):

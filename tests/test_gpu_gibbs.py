@@ -138,6 +138,17 @@ def test_cfg5_full_size():
     assert abs(tot[0] / nc - ex) < 6 * sd, (tot[0] / nc, ex)
     assert abs(tot[3] / nc - ey) < 6 * sd, (tot[3] / nc, ey)
     assert abs(tot[1] / nc - 1 / 18) < 1e-3 and abs(tot[6] / nc + 1 / 36) < 1e-3
+    # every moment total equals its per-chain definition (R-18) summed over the
+    # GPU's own chain statistics (bit-exact vs the oracle above) to 1e-12, and
+    # the between-chain ones (totals[2], [5], [7]) meet their exact expectations
+    # (tests/test_oracle_gibbs_moments.py)
+    st = g["chain_stats"]
+    mx, vx, my, vy, cxy = st
+    for idx, v in ((0, mx), (1, vx), (2, mx * mx), (3, my), (4, vy), (5, my * my),
+                   (6, cxy), (7, mx * my)):
+        assert abs(tot[idx] - math.fsum(v)) <= 1e-12 * abs(math.fsum(v)), idx
+    from tests.test_oracle_gibbs_moments import pin_failures
+    assert pin_failures(tot, st, ns, 0) == []
     # final x of 2^24 chains ~ marginal CDF 2x - x^2 (KS)
     from tests.stats_util import assert_ks_uniform
     fxv = g["final_xy"][0]
