@@ -212,7 +212,13 @@ BRNG_API int brng_gamma_f64(brng_t h, const double* alpha, const double* beta, d
  * alpha, out: row-major [n_rows][k].  Component (r, j) is Gamma sample
  * i = r*k + j of the contract above with beta = 1; S_r = sum_j y_rj (binary64,
  * any order); out[r][j] = y_rj / S_r rounded to the output type.  An invalid
- * component makes its whole row NaN.  trials: nullable u8[n_rows][k]. */
+ * component makes its whole row NaN.  trials: nullable u8[n_rows][k].
+ * Arithmetic: the kernels form fl(1/S_r) once per row and output
+ * y_rj * fl(1/S_r) (binary64) rounded to the output type; this is within one
+ * binary64 ulp of y_rj / S_r before that rounding, inside the parity
+ * tolerance (the oracle divides, as the definition states).  The sum is
+ * taken lane-strided then by a fixed shuffle tree: deterministic for given
+ * (alpha, k). */
 BRNG_API int brng_dirichlet_f32(brng_t h, const float* alpha, uint64_t n_rows, uint64_t k, float* out,
                        uint8_t* trials);
 BRNG_API int brng_dirichlet_f64(brng_t h, const double* alpha, uint64_t n_rows, uint64_t k, double* out,
@@ -234,8 +240,18 @@ BRNG_API int brng_dirichlet_f64(brng_t h, const double* alpha, uint64_t n_rows, 
  *                 [8] n_chains, [9] n_chains*(n_sweeps-burn_in), [10..15] 0,
  *                 [16+b] count of x samples with floor(256 x) = b (R-19).
  *                 Summation order is fixed for a given launch shape
- *                 (deterministic run to run).
- * A chain with y0 outside [0,1] (or NaN) yields NaN and is counted. */
+ *                 (deterministic run to run); a call chunked differently
+ *                 (host buffers) or sharded over ranks gives the same
+ *                 histogram and per-chain values but moment totals equal
+ *                 only to rounding (~1e-15 relative).
+ * A chain with y0 outside [0,1] (or NaN) yields NaN and is counted.
+ * Limits: n_sweeps < 2^22 (BRNG_ERR_SIZE otherwise: the per-CTA histogram
+ * counters are 32-bit, and a CTA round holds at most 768 chains, so a bin
+ * stays below 768 * 2^22 < 2^32 by construction); burn_in <= n_sweeps;
+ * stream_id + n_chains must not pass 2^64 (BRNG_ERR_OVERFLOW).
+ * Graph capture: the first call of a given chain count allocates the
+ * handle's partial-sum scratch and must run eagerly; inside a capture a call
+ * that would need a larger scratch returns BRNG_ERR_STATE. */
 BRNG_API int brng_gibbs_triangle(brng_t h, uint64_t n_chains, uint64_t n_sweeps, const double* x0,
                         const double* y0, uint64_t burn_in, double* out_x, double* out_y,
                         double* chain_stats, double* final_xy, double* totals);

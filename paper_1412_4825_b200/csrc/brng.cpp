@@ -9,8 +9,12 @@
 // stream, two staging slots), so PCIe transfers in both directions overlap
 // each other and the kernels.  Chunks are cut on sample (fills: Philox-block;
 // Dirichlet: row; Gibbs: chain) boundaries and every chunk is launched at the
-// cursor / stream its first unit has in the unchunked call, so results are
-// identical to a device-pointer call.
+// cursor / stream its first unit has in the unchunked call, so every sample,
+// per-chain statistic, final state and histogram count is identical to a
+// device-pointer call.  The Gibbs moment totals (totals[0..7]) are sums over
+// chains whose order depends on the chunking (each chunk's K7 sum is added to
+// the running totals), so they agree to rounding (~1e-15 relative), not bit
+// for bit.
 #include "../../include/brng.h"
 
 #include <cuda_runtime.h>
@@ -57,7 +61,11 @@ struct brng_handle_s {
   cudaEvent_t ev_in[kSlots], ev_k[kSlots], ev_out[kSlots];
   void* stage[kSlots];
   size_t stage_cap;
+  int stage_n;                 // slots allocated (at stage_cap bytes each)
   bool pipe_ready;
+  // scratch buffers replaced by a larger one stay allocated until
+  // brng_destroy: a CUDA graph captured earlier may still reference them
+  std::vector<void*> retired;
 };
 
 namespace {
@@ -157,7 +165,35 @@ bool trace_on() {
   return on;
 }
 
-int ensure_pipe(brng_t h, size_t slot_bytes) {
+// Stream-capture state of the handle's stream (scratch growth must not
+// synchronise or free inside a capture).
+bool capturing(brng_t h) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(h->stream, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs != cudaStreamCaptureStatusNone;
+}
+
+// Grow a handle-owned device scratch to at least `need` elements of `esize`
+// bytes.  The old buffer is retired (kept until brng_destroy), never freed
+// here, so graphs captured with it stay valid and no synchronisation is
+// needed.  Returns false when the allocation fails.
+bool grow_scratch(brng_t h, void** buf, size_t* cap, size_t need, size_t esize) {
+  if (need <= *cap) return true;
+  void* nb = nullptr;
+  if (cudaMalloc(&nb, need * esize) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (*buf) h->retired.push_back(*buf);
+  *buf = nb;
+  *cap = need;
+  return true;
+}
+
+int ensure_pipe(brng_t h, size_t slot_bytes, int n_slots) {
   if (!h->pipe_ready) {
     if (cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking) != cudaSuccess)
@@ -170,18 +206,24 @@ int ensure_pipe(brng_t h, size_t slot_bytes) {
       h->stage[b] = nullptr;
     }
     h->stage_cap = 0;
+    h->stage_n = 0;
     h->pipe_ready = true;
   }
+  // staging slots are reused across calls: earlier transfers on the copy
+  // streams must be done before a slot is freed
   if (slot_bytes > h->stage_cap) {
+    cudaStreamSynchronize(h->s_in);
+    cudaStreamSynchronize(h->s_out);
     for (int b = 0; b < kSlots; ++b) {
       if (h->stage[b]) cudaFree(h->stage[b]);
       h->stage[b] = nullptr;
     }
-    h->stage_cap = 0;
-    for (int b = 0; b < kSlots; ++b)
-      if (cudaMalloc(&h->stage[b], slot_bytes) != cudaSuccess) return BRNG_ERR_CUDA;
     h->stage_cap = slot_bytes;
+    h->stage_n = 0;
   }
+  // only as many slots as the call has chunks (a one-chunk call needs one)
+  for (; h->stage_n < n_slots; ++h->stage_n)
+    if (cudaMalloc(&h->stage[h->stage_n], h->stage_cap) != cudaSuccess) return BRNG_ERR_CUDA;
   return BRNG_OK;
 }
 
@@ -193,8 +235,13 @@ using Launch =
 // handle's stream (asynchronous).  Any host array: chunked pipeline; returns
 // after every host output is written.
 // max_units (0 = none) caps a chunk below the byte target.
+// soft_align: `align` is a performance preference (may be dropped), not a
+// counter-alignment requirement.
 int run(brng_t h, std::vector<Arr>& arrs, uint64_t n_units, uint64_t align, const Launch& launch,
-        uint64_t max_units = 0) {
+        uint64_t max_units = 0, bool soft_align = false) {
+  auto prefer_only_align_ok = [&](uint64_t al, size_t w) {
+    return !soft_align || (uint64_t)w <= kChunkBytes / al;
+  };
   bool any_host = false;
   for (auto& a : arrs) {
     a.host = a.ptr != nullptr && !is_device_ptr(a.ptr);
@@ -214,6 +261,10 @@ int run(brng_t h, std::vector<Arr>& arrs, uint64_t n_units, uint64_t align, cons
   size_t widest = 1;
   for (auto& a : arrs)
     if (a.host) widest = std::max(widest, a.unit_bytes * a.rows);
+  // an alignment that is only a performance preference (Gibbs: whole
+  // resident waves) is dropped when one aligned chunk would exceed the byte
+  // target (host out_x/out_y rows: a wave of chains x n_sweeps x 8 B)
+  if (align > 1 && !prefer_only_align_ok(align, widest)) align = 1;
   uint64_t chunk = std::max<uint64_t>(align, (kChunkBytes / widest) / align * align);
   if (max_units) chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(align, max_units / align * align));
   chunk = std::min<uint64_t>(chunk, n_units);
@@ -224,12 +275,12 @@ int run(brng_t h, std::vector<Arr>& arrs, uint64_t n_units, uint64_t align, cons
       slot += (a.unit_bytes * a.rows * chunk + 255) & ~size_t(255);
     }
   const auto t_beg = std::chrono::steady_clock::now();
-  int st = ensure_pipe(h, slot);
+  const uint64_t n_chunks = (n_units + chunk - 1) / chunk;
+  int st = ensure_pipe(h, slot, (int)std::min<uint64_t>(kSlots, n_chunks));
   if (st) return st;
   // the first copies must not overtake earlier work of this handle's stream
   cudaError_t e = cudaEventRecord(h->ev_k[0], h->stream);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(h->s_in, h->ev_k[0], 0);
-  const uint64_t n_chunks = (n_units + chunk - 1) / chunk;
   for (uint64_t j = 0; j < n_chunks && e == cudaSuccess; ++j) {
     const int b = (int)(j % kSlots);
     const uint64_t u0 = j * chunk, nu = std::min(chunk, n_units - u0);
@@ -371,22 +422,12 @@ int dirichlet_common(brng_t h, int dtype, const void* alpha, uint64_t n_rows, ui
   // handle-owned scratch (one row per resident warp) instead of recomputing
   // them; above 2 GB of scratch the kernel recomputes
   const size_t scr = brng::dirichlet_scratch_len(dtype, k, ctx);
+  // (no growth inside a stream capture: the rows are recomputed instead)
   if (scr && scr <= (size_t(1) << 28)) {
-    if (scr > h->dir_scratch_cap) {
-      if (h->d_dir_scratch) {
-        cudaStreamSynchronize(h->stream);
-        cudaFree(h->d_dir_scratch);
-        h->d_dir_scratch = nullptr;
-        h->dir_scratch_cap = 0;
-      }
-      if (cudaMalloc(&h->d_dir_scratch, scr * sizeof(double)) != cudaSuccess) {
-        cudaGetLastError();
-        h->d_dir_scratch = nullptr;       // fall back to recomputing the rows
-      } else {
-        h->dir_scratch_cap = scr;
-      }
-    }
-    ctx.dir_scratch = h->d_dir_scratch;
+    if (scr > h->dir_scratch_cap && !capturing(h))
+      grow_scratch(h, reinterpret_cast<void**>(&h->d_dir_scratch), &h->dir_scratch_cap, scr,
+                   sizeof(double));                 // failure: recompute the rows
+    if (scr <= h->dir_scratch_cap) ctx.dir_scratch = h->d_dir_scratch;
   }
   st = run(h, arrs, n_rows, 1, [&](uint64_t r0, uint64_t nr, const std::vector<void*>& d, bool) {
     return brng::launch_dirichlet(dtype, d[0], nr, k, d[1], static_cast<uint8_t*>(d[2]),
@@ -429,7 +470,7 @@ int brng_create(uint64_t seed, uint64_t stream_id, brng_t* out) {
   h->device = dev; h->num_sms = sms; h->stream = nullptr;
   h->d_partials = nullptr; h->partials_cap = 0; h->d_totals = nullptr;
   h->d_dir_scratch = nullptr; h->dir_scratch_cap = 0;
-  h->pipe_ready = false; h->stage_cap = 0;
+  h->pipe_ready = false; h->stage_cap = 0; h->stage_n = 0;
   if (cudaMalloc(&h->d_err, 2 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMemset(h->d_err, 0, 2 * sizeof(unsigned long long)) != cudaSuccess) {
     delete h;
@@ -453,6 +494,7 @@ int brng_destroy(brng_t h) {
   if (h->d_partials) cudaFree(h->d_partials);
   if (h->d_totals) cudaFree(h->d_totals);
   if (h->d_dir_scratch) cudaFree(h->d_dir_scratch);
+  for (void* p : h->retired) cudaFree(p);
   if (h->pipe_ready) {
     cudaStreamSynchronize(h->s_in);
     cudaStreamSynchronize(h->s_out);
@@ -599,7 +641,9 @@ int brng_gibbs_triangle(brng_t h, uint64_t n_chains, uint64_t n_sweeps, const do
                         double* chain_stats, double* final_xy, double* totals) {
   if (!h) return BRNG_ERR_NULL;
   if (burn_in > n_sweeps) return BRNG_ERR_SIZE;
-  if (n_sweeps >= (1ull << 23)) return BRNG_ERR_SIZE;   // u32 shared histogram bound
+  // u32 shared-memory histogram: a CTA round holds at most 768 chains, so
+  // < 768 * 2^22 < 2^32 counts per bin by construction
+  if (n_sweeps >= (1ull << 22)) return BRNG_ERR_SIZE;
   if (n_chains == 0) return BRNG_OK;
   if (!mul_ok(n_chains, n_sweeps) || !mul_ok(n_chains * n_sweeps, 8) || !mul_ok(n_chains, 40))
     return BRNG_ERR_SIZE;
@@ -612,14 +656,11 @@ int brng_gibbs_triangle(brng_t h, uint64_t n_chains, uint64_t n_sweeps, const do
   const Ctx ctx = make_ctx(h);
   const size_t need = brng::gibbs_partials_len(n_chains, ctx);
   if (need > h->partials_cap) {
-    if (h->d_partials) {
-      cudaStreamSynchronize(h->stream);
-      cudaFree(h->d_partials);
-      h->d_partials = nullptr;
-      h->partials_cap = 0;
-    }
-    if (cudaMalloc(&h->d_partials, need * sizeof(double)) != cudaSuccess) return BRNG_ERR_CUDA;
-    h->partials_cap = need;
+    // a capture cannot allocate: make one eager call of this size first
+    if (capturing(h)) return BRNG_ERR_STATE;
+    if (!grow_scratch(h, reinterpret_cast<void**>(&h->d_partials), &h->partials_cap, need,
+                      sizeof(double)))
+      return BRNG_ERR_CUDA;
   }
   // totals belongs to the call, not to a chain: a host totals pointer gets a
   // device scratch that every chunk accumulates into
@@ -627,6 +668,7 @@ int brng_gibbs_triangle(brng_t h, uint64_t n_chains, uint64_t n_sweeps, const do
   const bool host_tot = totals != nullptr && !is_device_ptr(totals);
   // (a handle-owned buffer, allocated once: a per-call cudaMallocAsync /
   // cudaFreeAsync pair was measured to stall some calls by 0.3-0.6 s)
+  if (host_tot && h->d_totals == nullptr && capturing(h)) return BRNG_ERR_STATE;
   if (host_tot && h->d_totals == nullptr &&
       cudaMalloc(reinterpret_cast<void**>(&h->d_totals), BRNG_TOTALS_LEN * 8) != cudaSuccess)
     return BRNG_ERR_CUDA;
@@ -656,7 +698,7 @@ int brng_gibbs_triangle(brng_t h, uint64_t n_chains, uint64_t n_sweeps, const do
                                        static_cast<double*>(d[4]), static_cast<double*>(d[5]),
                                        dtot, h->d_partials, base, cc, !first);
            },
-           BRNG_GIBBS_CHUNK_WAVES * wave);
+           BRNG_GIBBS_CHUNK_WAVES * wave, /*soft_align=*/true);
   if (host_tot) {
     cudaError_t e = cudaMemcpyAsync(totals, dtot, BRNG_TOTALS_LEN * 8, cudaMemcpyDeviceToHost,
                                     h->stream);

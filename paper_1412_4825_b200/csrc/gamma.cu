@@ -469,10 +469,14 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __gri
 
 // Any K: two passes over the row.  binary64 output: the first pass stores the
 // unnormalised Gammas in the output row itself, the second rescales them in
-// place (the same values as the shared-memory kernel).  binary32 output: a
-// Gamma may not be representable in binary32 before the division (a row of
-// tiny alphas), so the second pass recomputes it from its counters -- exact,
-// no scratch.
+// place.  binary32 output: a Gamma may not be representable in binary32
+// before the division (a row of tiny alphas), so the Gammas go to a
+// handle-owned binary64 scratch row per warp.  Both sum the row in the
+// shared-memory kernel's order (lane-strided, then the xor tree), so they
+// give the same values as it.  Without scratch (above 2 GB, or inside a graph
+// capture that would have to grow it) the second pass recomputes every Gamma
+// from its counters; that path sums in queue order (a deterministic order,
+// but not the shared-memory kernel's: values may differ in the last bit).
 template <typename T>
 __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(const __grid_constant__ DirArgs<T> a) {
   __shared__ BoostItem qs[kDirThreads / 32][kBoostCap];
@@ -501,29 +505,30 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(const __gr
       double* g_row = a.scratch + warp * a.k;
       mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
                [&](uint64_t i, double v, uint32_t t) {
-                 s += v;
                  g_row[i - beg] = v;
                  if (a.trials) a.trials[i] = (uint8_t)t;
                },
                nbad, q);
+      __syncwarp();                           // the row's Gammas are visible to the warp
+      const uint32_t lane = threadIdx.x & 31;
+      // the shared-memory kernel's sum order: lane-strided, then the xor tree
+      for (uint64_t j = lane; j < a.k; j += 32) s += g_row[j];
       s = warp_sum(s);
       const double inv = 1.0 / s;
-      __syncwarp();
-      const uint32_t lane = threadIdx.x & 31;
       for (uint64_t j = lane; j < a.k; j += 32) a.out[beg + j] = (T)(g_row[j] * inv);
       __syncwarp();
     } else if constexpr (sizeof(T) == 8) {
       mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
                [&](uint64_t i, double v, uint32_t t) {
-                 s += v;
                  a.out[i] = (T)v;
                  if (a.trials) a.trials[i] = (uint8_t)t;
                },
                nbad, q);
-      s = warp_sum(s);
-      const double inv = 1.0 / s;
       __syncwarp();                           // the row's stores are visible to the warp
       const uint32_t lane = threadIdx.x & 31;
+      for (uint64_t j = lane; j < a.k; j += 32) s += (double)a.out[beg + j];
+      s = warp_sum(s);
+      const double inv = 1.0 / s;
       for (uint64_t j = lane; j < a.k; j += 32) a.out[beg + j] = (T)((double)a.out[beg + j] * inv);
     } else {
       mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,

@@ -321,7 +321,9 @@ gibbs_kernel(GibbsArgs a) {
       const double v = warp_sum(t[j]);
       if (lane == 0) red[wid][j] += v;
     }
-    // drain the u32 shared histogram every round (< 512 * 2^23 = 2^32 counts)
+    // drain the u32 shared histogram every round: a round holds at most
+    // THREADS * CPT = 768 chains and the C ABI refuses n_sweeps >= 2^22, so a
+    // bin holds < 768 * 2^22 < 2^32 counts by construction
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kBinsPerThread; ++j) {

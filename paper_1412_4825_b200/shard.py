@@ -4,7 +4,10 @@ collective of the hot path.
 Samples, documents and chains are independent (Fig. 1
 is per chain), so the path shards by COUNTER RANGE with no data-path
 exchange: rank r draws exactly the samples an unsharded run would draw at the
-same indices, so every output is bit-identical for any GPU count.  The only
+same indices, so every sample, Dirichlet row, per-chain statistic, final state
+and histogram count is bit-identical for any GPU count.  The Gibbs moment
+totals (sums over chains) are added in a rank-dependent order and agree to
+rounding (~1e-15 relative), not bit for bit.  The only
 collective is the sum of the Gibbs totals (moment sums + 256-bin histogram,
 BASELINE.json configs[4]), done with torch.distributed (NCCL on B200, gloo
 in the CPU tests).

@@ -28,7 +28,7 @@ def test_error_codes_and_cursor_untouched():
         # burn_in > n_sweeps; n_sweeps beyond the histogram bound
         assert raw("brng_gibbs_triangle", h, 4, 3, None, None, 4, None, None, None, None,
                    None) == -2
-        assert raw("brng_gibbs_triangle", h, 4, 1 << 23, None, None, 0, None, None, None, None,
+        assert raw("brng_gibbs_triangle", h, 4, 1 << 22, None, None, 0, None, None, None, None,
                    None) == -2
         assert B.brng_get_offset(h) == 123
         # cursor overflow past 2^64 (Gamma reserves 256 blocks per sample)

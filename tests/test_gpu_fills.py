@@ -315,6 +315,27 @@ def test_batch_fill_equals_constant_arrays():
             B.brng_batch_fill(h, 5, 0, 0.0, 1.0, torch.empty(4, device=dev()), 4)
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_batch_fill_vs_oracle(dt):
+    """N1 (the VSL-Batch column; P:L7 vdRngUniform(method, stream, n,
+    r, a, b)): the fixed-parameter batch fill against the ORACLE fed constant
+    parameter arrays, element by element (ragged n, a cursor crossing 2^32
+    blocks, a nonzero stream), under the fills' parity tolerance."""
+    n = 40_009
+    base = (1 << 32) - 7000
+    code = 0 if dt == np.float32 else 1
+    td = torch.float32 if dt == np.float32 else torch.float64
+    for dist, (p0, p1) in {"uniform": (-1.0, 2.5), "gaussian": (1.0, 3.0),
+                           "exponential": (0.5, 0.0), "laplace": (2.0, 0.25),
+                           "weibull": (1.5, 2.0)}.items():
+        with handle(31, 4, base) as h:
+            ob = torch.empty(n, dtype=td, device=dev())
+            B.brng_batch_fill(h, B.DIST[dist], code, p0, p1, ob, n)
+        params = [np.full(n, p0, dt)] + ([] if dist == "exponential" else [np.full(n, p1, dt)])
+        ref, scale = parity.fill_reference(dist, 31, 4, base, params, 0, dt)
+        parity.check_close(ob, ref, scale, dt, f"batch {dist} {np.dtype(dt).name}")
+
+
 @pytest.mark.slow
 def test_fill_beyond_2_31_samples():
     """64-bit indexing: n = 2^31 + 7 f32 uniforms (8.6 GB per array); sampled

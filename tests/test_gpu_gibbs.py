@@ -167,6 +167,21 @@ def test_host_pipeline_multi_chunk_gibbs():
     np.testing.assert_allclose(tot[:HDR], g["totals"][:HDR], rtol=1e-12)
 
 
+def test_host_samples_more_chains_than_a_wave():
+    """Host out_x/out_y with more chains than one resident wave: the staging
+    chunk is capped by bytes (a wave of chains x 64 sweeps x 8 B would exceed
+    the 64 MB target), and the samples equal a device-pointer call bit for bit."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    nc, ns = 2 * 256 * 3 * sms + 1017, 64                 # > one bulk wave
+    g = _run(42, 0, 0, nc, ns, samples=True)
+    ox = np.empty((ns, nc)); oy = np.empty((ns, nc)); st = np.empty((5, nc))
+    with handle(42) as h:
+        B.brng_gibbs_triangle(h, nc, ns, None, None, 0, ox, oy, st, None, None)
+        assert B.brng_get_offset(h) == ns
+    assert np.array_equal(ox, g["out_x"]) and np.array_equal(oy, g["out_y"])
+    assert np.array_equal(st, g["chain_stats"])
+
+
 def test_launch_shapes_agree_across_the_latency_threshold():
     """Three launch shapes serve different chain counts (chain/helper warp
     pairs up to 32 chains per SM, thread per chain below half a bulk wave,

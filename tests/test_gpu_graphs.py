@@ -62,3 +62,50 @@ def test_graph_replay_equals_eager():
             assert B.brng_device_errors(h) == 0
     finally:
         B.brng_destroy(h)
+
+
+def test_graph_survives_scratch_growth():
+    """A graph captured with a large-K binary32 Dirichlet (handle scratch rows)
+    stays valid after a later eager call on the same handle grows that scratch
+    (the old buffer is retired, not freed), and a capture never allocates."""
+    dev = torch.device("cuda:0")
+    a1 = workloads.cfg4_params(40, 2048, seed=3, device=dev)
+    a2 = workloads.cfg4_params(20, 4096, seed=4, device=dev)
+    o1 = torch.empty(40, 2048, device=dev)
+    o2 = torch.empty(20, 4096, device=dev)
+    s = torch.cuda.Stream()
+    h = B.brng_create(5, 0)
+    try:
+        with torch.cuda.stream(s):
+            B.brng_set_cuda_stream(h, s.cuda_stream)
+            B.brng_set_offset(h, 0)
+            B.brng_dirichlet_f32(h, a1, 40, 2048, o1, None)      # eager: scratch for K = 2048
+            s.synchronize()
+            eager = o1.clone()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=s):
+                B.brng_set_offset(h, 0)
+                B.brng_dirichlet_f32(h, a1, 40, 2048, o1, None)
+            B.brng_dirichlet_f32(h, a2, 20, 4096, o2, None)      # eager: grows the scratch
+            s.synchronize()
+            o1.fill_(-1.0)
+            graph.replay()
+            s.synchronize()
+            assert torch.equal(o1, eager)
+            # a capture that would need more scratch recomputes the rows instead
+            g2 = torch.cuda.CUDAGraph()
+            a3 = workloads.cfg4_params(8, 8192, seed=5, device=dev)
+            o3 = torch.empty(8, 8192, device=dev)
+            with torch.cuda.graph(g2, stream=s):
+                B.brng_set_offset(h, 0)
+                B.brng_dirichlet_f32(h, a3, 8, 8192, o3, None)
+            g2.replay()
+            s.synchronize()
+            B.brng_set_offset(h, 0)
+            ref = torch.empty_like(o3)
+            B.brng_dirichlet_f32(h, a3, 8, 8192, ref, None)      # eager, with scratch
+            s.synchronize()
+            torch.testing.assert_close(o3, ref, rtol=2e-6, atol=0)
+            assert B.brng_device_errors(h) == 0
+    finally:
+        B.brng_destroy(h)

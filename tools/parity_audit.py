@@ -9,10 +9,11 @@ against the parity tolerance.  Also every cfg2 sample (both fills) against
 the oracle's value, and every cfg5 chain's statistics and final state
 (bit-exact) and the histogram (exact).  Prints one JSON object.
 
-usage: python tools/decision_audit.py > profiles/r01_parity_audit.json
+usage: python tools/parity_audit.py > profiles/r02_parity_audit.json
 """
 import json
 import os
+import threading
 import sys
 import time
 
@@ -79,24 +80,21 @@ def audit_cfg3(P):
     t_or = time.perf_counter() - t0
     nd, nt, nf = classify(t, tref, a, seed, lambda k: int(k))
     same = t == tref
-    ratio = max_ratio(g[same], ref[same], np.abs(ref[same]), np.float64, seed, a[same],
-                      tref[same], np.flatnonzero(same))
+    vc = max_ratio(g[same], ref[same], np.abs(ref[same]), np.float64, seed, a[same],
+                   tref[same], np.flatnonzero(same))
     return dict(n=n, device_errors=errs, disagreements=nd, ties=nt, fails=nf,
-                tie_rate=nt / n, max_value_error_ratio=ratio, oracle_s=round(t_or, 2))
+                tie_rate=nt / n, max_value_error_ratio=vc.pop("ratio"), values=vc,
+                oracle_s=round(t_or, 2))
 
 
 def max_ratio(got, ref, scale, dtype, seed, alpha, tref, idx):
-    """Max |got-ref| / (tau scale + eps); the conditioning factor of the
-    accepting trial is applied where the plain bound is exceeded
-    (tests/parity.py)."""
-    tau, eps = parity.TAU[np.dtype(dtype)], parity.EPS_MIN[np.dtype(dtype)]
-    err = np.abs(got.astype(np.float64) - ref.astype(np.float64))
-    bound = tau * scale + eps
-    loose = np.flatnonzero(err > bound)
-    for k in loose:
-        bound[k] *= max(1.0, parity.gamma_condition(seed, 0, 0, int(idx[k]), float(alpha[k]),
-                                                    int(tref[k])))
-    return float(np.max(err / bound)) if err.size else 0.0
+    """The value criterion of tests/parity.py (value_check): max error / bound
+    plus how many samples needed each relaxation -- the tau * smallest-normal
+    floor, the Marsaglia-Tsang condition factor -- and the worst plain
+    relative error |x - x_ref| / |x_ref|."""
+    return parity.value_check(got, ref, scale, dtype,
+                              lambda k: parity.gamma_condition(seed, 0, 0, int(idx[k]),
+                                                               float(alpha[k]), int(tref[k])))
 
 
 def audit_cfg4(P):
@@ -128,12 +126,13 @@ def audit_cfg4(P):
     nd, nt, nf = classify(tf, tref_f, af, seed, lambda k: int(k))
     # values: rows without any disagreement (a tie moves the whole row's sum)
     row_ok = (t == tref).all(axis=1)
-    ratio = max_ratio(x[row_ok].reshape(-1), ref[row_ok].reshape(-1),
-                      np.abs(ref[row_ok].reshape(-1).astype(np.float64)), np.float32, seed,
-                      a[row_ok].reshape(-1), tref[row_ok].reshape(-1),
-                      np.flatnonzero(np.repeat(row_ok, K)))
+    vc = max_ratio(x[row_ok].reshape(-1), ref[row_ok].reshape(-1),
+                   np.abs(ref[row_ok].reshape(-1).astype(np.float64)), np.float32, seed,
+                   a[row_ok].reshape(-1), tref[row_ok].reshape(-1),
+                   np.flatnonzero(np.repeat(row_ok, K)))
     return dict(n=D * K, rows=D, device_errors=errs, disagreements=nd, ties=nt, fails=nf,
-                tie_rate=nt / (D * K), max_value_error_ratio=ratio, oracle_s=round(t_or, 2))
+                tie_rate=nt / (D * K), max_value_error_ratio=vc.pop("ratio"), values=vc,
+                oracle_s=round(t_or, 2))
 
 
 def audit_cfg2(P):
@@ -142,6 +141,7 @@ def audit_cfg2(P):
     dev = torch.device("cuda:0")
     p = W.cfg2_params(n, seed=seed, device=dev)
     res = {}
+    lock = threading.Lock()
     for dist, keys in (("gaussian", ("mu", "sigma")), ("uniform", ("a", "b"))):
         out = torch.empty(n, device=dev)
         h = B.brng_create(seed, 0)
@@ -151,20 +151,22 @@ def audit_cfg2(P):
         B.brng_destroy(h)
         got = out.cpu().numpy()
         p0, p1 = p[keys[0]].cpu().numpy(), p[keys[1]].cpu().numpy()
-        worst = [0.0]
+        agg = dict(ratio=0.0, n=0, worst_plain_rel=0.0, n_plain_fail=0, n_floor=0, n_cond=0)
         chunk = 1 << 22
 
         def fn(lo, hi):
             ref, scale = parity.fill_reference(dist, seed, 0, 0, [p0[lo:hi], p1[lo:hi]], lo,
                                                np.float32)
-            err = np.abs(got[lo:hi].astype(np.float64) - ref.astype(np.float64))
-            r = float(np.max(err / (parity.TAU[np.dtype(np.float32)] * scale +
-                                    parity.EPS_MIN[np.dtype(np.float32)])))
-            worst[0] = max(worst[0], r)
+            vc = parity.value_check(got[lo:hi], ref, scale, np.float32, None, dist)
+            with lock:
+                for k in ("ratio", "worst_plain_rel"):
+                    agg[k] = max(agg[k], vc[k])
+                for k in ("n", "n_plain_fail", "n_floor", "n_cond"):
+                    agg[k] += vc[k]
         t0 = time.perf_counter()
         oracle.run_parallel(fn, [(lo, min(lo + chunk, n)) for lo in range(0, n, chunk)], P)
-        res[dist] = dict(n=n, device_errors=errs, max_value_error_ratio=worst[0],
-                         oracle_s=round(time.perf_counter() - t0, 2))
+        res[dist] = dict(n=n, device_errors=errs, max_value_error_ratio=agg.pop("ratio"),
+                         values=agg, oracle_s=round(time.perf_counter() - t0, 2))
     return res
 
 
@@ -206,6 +208,13 @@ def main():
     P = cores()
     r = {"cores": P, "cfg3_gamma_f64": audit_cfg3(P), "cfg4_dirichlet_f32": audit_cfg4(P),
          "cfg2_fills_f32": audit_cfg2(P), "cfg5_gibbs": audit_cfg5(P)}
+    r["values_legend"] = ("n: values compared; worst_plain_rel: max |x-x_ref|/|x_ref|; "
+                          "n_plain_fail: outside tau*|x_ref| + one subnormal (SURVEY 8c.5 "
+                          "literal, scale |x_ref|); n_floor: rescued by the tau*smallest-normal "
+                          "floor alone; n_cond: needed the Marsaglia-Tsang condition factor "
+                          "3|cz/(1+cz)| (Gamma/Dirichlet) -- for the fills scale is "
+                          "|mu|+|sigma z| / |a|+|b-a|u, so n_cond counts samples outside "
+                          "that bound (must be 0)")
     r["criterion"] = ("decisions: every sample's accepting trial equals the oracle's except "
                       "ties (oracle margin within 1e-10 max(1,d) or |1+cz| <= 1e-10); ties "
                       "< 1e-6 of draws; values within the parity tolerance (ratio <= 1); Gibbs "
