@@ -133,7 +133,7 @@ def value_check(got, ref, scale, dtype, cond_at=None, what="values"):
     Bound = tau * scale * cond + EPS_MIN, where cond = cond_at(k) (the
     Marsaglia-Tsang condition number, Gamma/Dirichlet) is applied only where
     the plain bound tau * scale + EPS_MIN fails.  Returns dict(ratio = max
-    error / bound (must be <= 1), n = values compared, worst_plain_rel = max
+    error / bound (must be <= 1), n_values = values compared, worst_plain_rel = max
     |x - x_ref| / |x_ref| over x_ref != 0, n_plain_fail = samples outside the
     literal SURVEY 8c.5 bound tau |x_ref| + one subnormal, n_floor = those
     rescued by the tau * smallest-normal floor alone, n_cond = those that
@@ -162,7 +162,7 @@ def value_check(got, ref, scale, dtype, cond_at=None, what="values"):
     if ratio > 1.0:
         k = int(np.argmax(err / bound))
         raise AssertionError(f"{what}: error ratio {ratio:.3g}: got {got[k]!r} ref {ref[k]!r}")
-    return dict(ratio=ratio, n=int(err.size), worst_plain_rel=worst_plain,
+    return dict(ratio=ratio, n_values=int(err.size), worst_plain_rel=worst_plain,
                 n_plain_fail=int(np.count_nonzero(plain_fail)), n_floor=n_floor,
                 n_cond=int(np.count_nonzero(loose)))
 

@@ -151,7 +151,7 @@ def audit_cfg2(P):
         B.brng_destroy(h)
         got = out.cpu().numpy()
         p0, p1 = p[keys[0]].cpu().numpy(), p[keys[1]].cpu().numpy()
-        agg = dict(ratio=0.0, n=0, worst_plain_rel=0.0, n_plain_fail=0, n_floor=0, n_cond=0)
+        agg = dict(ratio=0.0, n_values=0, worst_plain_rel=0.0, n_plain_fail=0, n_floor=0, n_cond=0)
         chunk = 1 << 22
 
         def fn(lo, hi):
@@ -161,7 +161,7 @@ def audit_cfg2(P):
             with lock:
                 for k in ("ratio", "worst_plain_rel"):
                     agg[k] = max(agg[k], vc[k])
-                for k in ("n", "n_plain_fail", "n_floor", "n_cond"):
+                for k in ("n_values", "n_plain_fail", "n_floor", "n_cond"):
                     agg[k] += vc[k]
         t0 = time.perf_counter()
         oracle.run_parallel(fn, [(lo, min(lo + chunk, n)) for lo in range(0, n, chunk)], P)
@@ -208,7 +208,7 @@ def main():
     P = cores()
     r = {"cores": P, "cfg3_gamma_f64": audit_cfg3(P), "cfg4_dirichlet_f32": audit_cfg4(P),
          "cfg2_fills_f32": audit_cfg2(P), "cfg5_gibbs": audit_cfg5(P)}
-    r["values_legend"] = ("n: values compared; worst_plain_rel: max |x-x_ref|/|x_ref|; "
+    r["values_legend"] = ("n_values: values compared; worst_plain_rel: max |x-x_ref|/|x_ref|; "
                           "n_plain_fail: outside tau*|x_ref| + one subnormal (SURVEY 8c.5 "
                           "literal, scale |x_ref|); n_floor: rescued by the tau*smallest-normal "
                           "floor alone; n_cond: needed the Marsaglia-Tsang condition factor "
