@@ -61,6 +61,7 @@ struct GibbsArgs {
   uint64_t n_chains, base, stream_id;
   uint32_t n_sweeps, burn_in;   // n_sweeps < 2^23 (host-checked; u32 histogram)
   uint32_t rounds;              // grid-stride rounds (kCPT chains per thread each)
+  uint32_t tail_rounds;         // then rounds of one chain per thread (bulk kernel)
   uint32_t rk0[10], rk1[10];    // Philox round keys k + r*W (kernel constants)
   uint32_t c3k1_u;              // UHI launches: hi32(stream) ^ k1, the same for every chain
   const double* x0;
@@ -236,10 +237,98 @@ __device__ __forceinline__ double warp_sum(double s) {
   return s;
 }
 
+// One round of a CTA: each thread runs CPT chains, chain k of thread t being
+// c0 + k * THREADS + t; then their statistics, the fixed-order round sums and
+// the histogram drain.
+template <bool STORE, int CPT, int THREADS, bool UHI, int KB>
+__device__ __forceinline__ void gibbs_round(const GibbsArgs& a, const RoundKeys& rk, uint64_t c0,
+                                            uint32_t* hist, double (*red)[8], double (&bins)[KB],
+                                            uint32_t& nbad, uint32_t hist_base) {
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  const double n = (double)(a.n_sweeps - a.burn_in);
+  const double nm1 = __dsub_rn(n, 1.0);
+  Chain ch[CPT];
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    Chain& q = ch[k];
+    q.c = c0 + (uint64_t)k * THREADS + threadIdx.x;
+    const bool real = q.c < a.n_chains;
+    const double x = (real && a.x0) ? a.x0[q.c] : 0.5;
+    const double y = (real && a.y0) ? a.y0[q.c] : 0.5;
+    const bool valid = (y >= 0.0) && (y <= 1.0);
+    q.live = real && valid;
+    nbad += (real && !valid);
+    q.X = __dmul_rn(x, kScale);
+    q.Y = __dmul_rn(valid ? y : qnan, kScale);
+    q.S1X = q.S2X = q.S1Y = q.S2Y = q.SXY = 0.0;
+  }
+  // one chain per thread (latency-bound small launches, the bulk tail):
+  // unroll deeper so the Philox blocks of several sweeps overlap the serial
+  // x/y update chain
+  constexpr int U = CPT == 1 ? kSmallUnroll : kUnroll;
+  sweeps<STORE, false, CPT, U, UHI>(a, rk, 0, a.burn_in, ch, hist_base);
+  sweeps<STORE, true, CPT, U, UHI>(a, rk, a.burn_in, a.n_sweeps, ch, hist_base);
+
+  double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    const Chain& q = ch[k];
+    if (q.c >= a.n_chains) continue;
+    const double s1x = __dmul_rn(q.S1X, kInvScale), s1y = __dmul_rn(q.S1Y, kInvScale);
+    const double s2x = __dmul_rn(q.S2X, kInvScale2), s2y = __dmul_rn(q.S2Y, kInvScale2);
+    const double sxy = __dmul_rn(q.SXY, kInvScale2);
+    const double mx = __ddiv_rn(s1x, n), my = __ddiv_rn(s1y, n);
+    const double vx = __ddiv_rn(__dsub_rn(s2x, __dmul_rn(s1x, mx)), nm1);
+    const double vy = __ddiv_rn(__dsub_rn(s2y, __dmul_rn(s1y, my)), nm1);
+    const double cxy = __ddiv_rn(__dsub_rn(sxy, __dmul_rn(s1x, my)), nm1);
+    const double fx = __dmul_rn(q.X, kInvScale), fy = __dmul_rn(q.Y, kInvScale);
+    if (a.chain_stats) {
+      a.chain_stats[0 * a.n_chains + q.c] = mx;
+      a.chain_stats[1 * a.n_chains + q.c] = vx;
+      a.chain_stats[2 * a.n_chains + q.c] = my;
+      a.chain_stats[3 * a.n_chains + q.c] = vy;
+      a.chain_stats[4 * a.n_chains + q.c] = cxy;
+    }
+    if (a.final_xy) { a.final_xy[q.c] = fx; a.final_xy[a.n_chains + q.c] = fy; }
+    if (STORE && !q.live) {             // invalid start: NaN samples (oracle semantics)
+      for (uint32_t s = 0; s < a.n_sweeps; ++s) {
+        if (a.out_x) a.out_x[(uint64_t)s * a.n_chains + q.c] = qnan;
+        if (a.out_y) a.out_y[(uint64_t)s * a.n_chains + q.c] = qnan;
+      }
+    }
+    t[0] += mx; t[1] += vx; t[2] += mx * mx; t[3] += my; t[4] += vy; t[5] += my * my;
+    t[6] += cxy; t[7] += mx * my;
+  }
+  // fixed-order reduction of this round's chain-level sums (warp tree, then
+  // lane 0 accumulates across rounds in order)
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double v = warp_sum(t[j]);
+    if (lane == 0) red[wid][j] += v;
+  }
+  // drain the u32 shared histogram every round: a round holds at most
+  // THREADS * CPT = 768 chains and the C ABI refuses n_sweeps >= 2^22, so a
+  // bin holds < 768 * 2^22 < 2^32 counts by construction
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < KB; ++j) {
+    bins[j] += (double)hist[threadIdx.x + j * THREADS];
+    hist[threadIdx.x + j * THREADS] = 0;
+  }
+  __syncthreads();
+}
+
 // THREADS threads x CPT chains per thread.  The bulk configuration is
 // <.., kCPT, kThreads> (kCPT = 3 chains per thread for ILP); small chain counts
 // (cfg1: 1024 chains) use one chain per thread in 64-thread CTAs to spread
 // the latency-bound chains over more SMs.
+// Bulk launches are one full resident wave: a.rounds rounds of CPT chains per
+// thread, then a.tail_rounds rounds of ONE chain per thread for the chains
+// left over.  The tail is what keeps the wave full when the chain count is
+// not a multiple of a wave (strong scaling: 2^24 / 8 GPUs = 9.2 waves): a
+// one-chain round costs about a third of a three-chain round, so the last
+// partial wave costs its size rounded up to a third, not a whole round.
 template <bool STORE, int CPT, int THREADS, bool UHI>
 __global__ void __launch_bounds__(THREADS, (THREADS == kThreads ? BRNG_GIBBS_MINB : 1))
 gibbs_kernel(GibbsArgs a) {
@@ -255,82 +344,21 @@ gibbs_kernel(GibbsArgs a) {
 #pragma unroll
   for (int j = 0; j < kBinsPerThread; ++j) bins[j] = 0.0;
   uint32_t nbad = 0;
-  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-  const double n = (double)(a.n_sweeps - a.burn_in);
-  const double nm1 = __dsub_rn(n, 1.0);
   const RoundKeys rk = load_keys(a);
   __syncthreads();
 
   const uint64_t per_round = (uint64_t)gridDim.x * THREADS * CPT;
-  for (uint32_t rnd = 0; rnd < a.rounds; ++rnd) {
-    Chain ch[CPT];
-#pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-      Chain& q = ch[k];
-      q.c = (uint64_t)rnd * per_round + ((uint64_t)blockIdx.x * CPT + k) * THREADS + threadIdx.x;
-      const bool real = q.c < a.n_chains;
-      const double x = (real && a.x0) ? a.x0[q.c] : 0.5;
-      const double y = (real && a.y0) ? a.y0[q.c] : 0.5;
-      const bool valid = (y >= 0.0) && (y <= 1.0);
-      q.live = real && valid;
-      nbad += (real && !valid);
-      q.X = __dmul_rn(x, kScale);
-      q.Y = __dmul_rn(valid ? y : qnan, kScale);
-      q.S1X = q.S2X = q.S1Y = q.S2Y = q.SXY = 0.0;
-    }
-    // one chain per thread (latency-bound small launches): unroll deeper so
-    // the Philox blocks of several sweeps overlap the serial x/y update chain
-    constexpr int U = CPT == 1 ? kSmallUnroll : kUnroll;
-    sweeps<STORE, false, CPT, U, UHI>(a, rk, 0, a.burn_in, ch, hist_base);
-    sweeps<STORE, true, CPT, U, UHI>(a, rk, a.burn_in, a.n_sweeps, ch, hist_base);
-
-    double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-      const Chain& q = ch[k];
-      if (q.c >= a.n_chains) continue;
-      const double s1x = __dmul_rn(q.S1X, kInvScale), s1y = __dmul_rn(q.S1Y, kInvScale);
-      const double s2x = __dmul_rn(q.S2X, kInvScale2), s2y = __dmul_rn(q.S2Y, kInvScale2);
-      const double sxy = __dmul_rn(q.SXY, kInvScale2);
-      const double mx = __ddiv_rn(s1x, n), my = __ddiv_rn(s1y, n);
-      const double vx = __ddiv_rn(__dsub_rn(s2x, __dmul_rn(s1x, mx)), nm1);
-      const double vy = __ddiv_rn(__dsub_rn(s2y, __dmul_rn(s1y, my)), nm1);
-      const double cxy = __ddiv_rn(__dsub_rn(sxy, __dmul_rn(s1x, my)), nm1);
-      const double fx = __dmul_rn(q.X, kInvScale), fy = __dmul_rn(q.Y, kInvScale);
-      if (a.chain_stats) {
-        a.chain_stats[0 * a.n_chains + q.c] = mx;
-        a.chain_stats[1 * a.n_chains + q.c] = vx;
-        a.chain_stats[2 * a.n_chains + q.c] = my;
-        a.chain_stats[3 * a.n_chains + q.c] = vy;
-        a.chain_stats[4 * a.n_chains + q.c] = cxy;
-      }
-      if (a.final_xy) { a.final_xy[q.c] = fx; a.final_xy[a.n_chains + q.c] = fy; }
-      if (STORE && !q.live) {             // invalid start: NaN samples (oracle semantics)
-        for (uint32_t s = 0; s < a.n_sweeps; ++s) {
-          if (a.out_x) a.out_x[(uint64_t)s * a.n_chains + q.c] = qnan;
-          if (a.out_y) a.out_y[(uint64_t)s * a.n_chains + q.c] = qnan;
-        }
-      }
-      t[0] += mx; t[1] += vx; t[2] += mx * mx; t[3] += my; t[4] += vy; t[5] += my * my;
-      t[6] += cxy; t[7] += mx * my;
-    }
-    // fixed-order reduction of this round's chain-level sums (warp tree, then
-    // lane 0 accumulates across rounds in order)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const double v = warp_sum(t[j]);
-      if (lane == 0) red[wid][j] += v;
-    }
-    // drain the u32 shared histogram every round: a round holds at most
-    // THREADS * CPT = 768 chains and the C ABI refuses n_sweeps >= 2^22, so a
-    // bin holds < 768 * 2^22 < 2^32 counts by construction
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kBinsPerThread; ++j) {
-      bins[j] += (double)hist[threadIdx.x + j * THREADS];
-      hist[threadIdx.x + j * THREADS] = 0;
-    }
-    __syncthreads();
+  for (uint32_t rnd = 0; rnd < a.rounds; ++rnd)
+    gibbs_round<STORE, CPT, THREADS, UHI>(
+        a, rk, (uint64_t)rnd * per_round + (uint64_t)blockIdx.x * CPT * THREADS, hist, red, bins,
+        nbad, hist_base);
+  if (CPT > 1) {
+    const uint64_t tail0 = (uint64_t)a.rounds * per_round;
+    const uint64_t per_tail = (uint64_t)gridDim.x * THREADS;
+    for (uint32_t rnd = 0; rnd < a.tail_rounds; ++rnd)
+      gibbs_round<STORE, 1, THREADS, UHI>(
+          a, rk, tail0 + (uint64_t)rnd * per_tail + (uint64_t)blockIdx.x * THREADS, hist, red,
+          bins, nbad, hist_base);
   }
 
   double* part = a.partials + (uint64_t)blockIdx.x * kTot;
@@ -637,14 +665,21 @@ int ctas_per_sm_lat() {
 #endif
 
 // Launch shape: `threads` x `cpt` chains per CTA per round, one resident wave
-// of CTAs; each thread runs `rounds` rounds so chains divide evenly.
+// of CTAs.  Small launches: each thread runs `rounds` rounds so chains divide
+// evenly.  Bulk launches: the full wave runs floor(n / wave) three-chain
+// rounds, and the remainder in one-chain tail rounds when that is cheaper
+// (at most 2 of them, ~2/3 of a round) than one more padded three-chain round.
 struct Shape {
   unsigned grid;
-  uint32_t rounds;
+  uint32_t rounds, tail_rounds;
   bool small;
 };
+#ifndef BRNG_GIBBS_TAIL
+#define BRNG_GIBBS_TAIL 1
+#endif
 inline Shape grid_shape(uint64_t n_chains, const Ctx& ctx) {
   Shape sh;
+  sh.tail_rounds = 0;
   const uint64_t bulk_wave = (uint64_t)ctx.num_sms * ctas_per_sm_bulk() * kThreads * kCPT;
   sh.small = n_chains < bulk_wave / 2;
   const int threads = sh.small ? kSmallThreads : kThreads;
@@ -652,6 +687,18 @@ inline Shape grid_shape(uint64_t n_chains, const Ctx& ctx) {
   const uint64_t max_ctas =
       (uint64_t)ctx.num_sms * (sh.small ? ctas_per_sm_small() : ctas_per_sm_bulk());
   const uint64_t per_round_max = max_ctas * threads * cpt;
+  if (!sh.small && BRNG_GIBBS_TAIL && kCPT > 1) {
+    const uint64_t full = n_chains / per_round_max;
+    const uint64_t rem = n_chains - full * per_round_max;
+    const uint64_t per_tail = max_ctas * threads;
+    const uint64_t tail = (rem + per_tail - 1) / per_tail;
+    if (tail <= 2) {
+      sh.grid = (unsigned)max_ctas;
+      sh.rounds = (uint32_t)full;
+      sh.tail_rounds = (uint32_t)tail;
+      return sh;
+    }
+  }
   const uint64_t r = (n_chains + per_round_max - 1) / per_round_max;
   sh.rounds = (uint32_t)(r ? r : 1);
   const uint64_t per_cta = (uint64_t)sh.rounds * threads * cpt;
@@ -684,6 +731,7 @@ cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
   const uint32_t rounds = sh.rounds;
   a.n_chains = n_chains; a.base = base; a.stream_id = ctx.stream_id;
   a.n_sweeps = (uint32_t)n_sweeps; a.burn_in = (uint32_t)burn_in; a.rounds = rounds;
+  a.tail_rounds = sh.tail_rounds;
   for (int r = 0; r < 10; ++r) {
     a.rk0[r] = ctx.k0 + (uint32_t)r * kPhiloxW0;
     a.rk1[r] = ctx.k1 + (uint32_t)r * kPhiloxW1;

@@ -182,6 +182,20 @@ def test_host_samples_more_chains_than_a_wave():
     assert np.array_equal(st, g["chain_stats"])
 
 
+@pytest.mark.parametrize("extra", [0.66, 1.2, 1.5])
+def test_bulk_tail_rounds_match_oracle(extra):
+    """Bulk launches whose chain count is not a multiple of a resident wave run
+    full three-chain rounds plus one-chain tail rounds (gibbs.cu grid_shape;
+    strong scaling 2^24 / 8 = 9.2 waves): every chain's statistics and final
+    state equal the oracle's, the histogram equals the oracle's exactly."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    wave = 2 * 256 * 3 * sms
+    nc, ns = int(extra * wave) + 7, 6
+    g = _run(42, 3, 11, nc, ns, samples=False)
+    r = oracle.gibbs_triangle(42, 3, 11, nc, ns, want_samples=False)
+    _assert_match(g, r, samples=False)
+
+
 def test_launch_shapes_agree_across_the_latency_threshold():
     """Three launch shapes serve different chain counts (chain/helper warp
     pairs up to 32 chains per SM, thread per chain below half a bulk wave,

@@ -32,7 +32,8 @@ if what == "gibbs1":
         B.brng_gibbs_triangle(h, nc, ns, None, None, 0, ox, oy, None, None, tot)
     outs = [ox, oy, tot[16:]]
 elif what == "gibbs":
-    nc, ns = 1 << 24, 4096
+    import os
+    nc, ns = int(os.environ.get("GIBBS_NC", 1 << 24)), 4096
     st = torch.empty(5, nc, dtype=torch.float64, device=dev)
     fx = torch.empty(2, nc, dtype=torch.float64, device=dev)
     tot = torch.empty(B.TOTALS_LEN, dtype=torch.float64, device=dev)
