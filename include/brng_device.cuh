@@ -327,11 +327,18 @@ __device__ __forceinline__ bool mt_exact(double z, double d, double v, uint32_t 
 // (~0.1% of trials) re-run the exact binary64 test in the contract's
 // operation order.  Decisions are therefore the binary64 contract's.
 // d is returned; alpha is consumed only after z (hides its load latency).
+// The trial splits into its parameter-free part (the standard normal z of the
+// block: the paper's buffered Gaussian) and the part that uses the
+// sample's alpha; mt_trial is exactly their composition, so a consumer that
+// gets z (and the block's word w3) from a producer's buffer (NEXT row N4,
+// reading R-33) computes the same decision and value bit for bit.
 template <class Tab = dm::GlobalTables>
-__device__ __forceinline__ bool mt_trial(uint4 w, double alpha, double& d, double& g,
-                                         const Tab& tb = Tab()) {
+__device__ __forceinline__ double mt_normal(uint4 w, const Tab& tb = Tab()) {
   const double L = dm::ln_pos(dm::one_minus_u53(w.x, w.y), tb);
-  const double z = __dmul_rn(dm::sqrt_nonneg(-2.0 * L), dm::cos2pi_u32(w.z, tb));
+  return __dmul_rn(dm::sqrt_nonneg(-2.0 * L), dm::cos2pi_u32(w.z, tb));
+}
+__device__ __forceinline__ bool mt_accept_z(double z, uint32_t w3, double alpha, double& d,
+                                            double& g) {
   double c;
   mt_consts(alpha, d, c);
   const double cz = __dmul_rn(c, z);
@@ -339,15 +346,31 @@ __device__ __forceinline__ bool mt_trial(uint4 w, double alpha, double& d, doubl
   if (!(t > 0.0)) return false;
   const double v = __dmul_rn(__dmul_rn(t, t), t);
   g = __dmul_rn(d, v);
-  const int sc = mt_screen(z, d, t, w.w);
+  const int sc = mt_screen(z, d, t, w3);
   if (sc != 0) return sc > 0;
-  return mt_exact(z, d, v, w.w);
+  return mt_exact(z, d, v, w3);
+}
+template <class Tab = dm::GlobalTables>
+__device__ __forceinline__ bool mt_trial(uint4 w, double alpha, double& d, double& g,
+                                         const Tab& tb = Tab()) {
+  return mt_accept_z(mt_normal(w, tb), w.w, alpha, d, g);
+}
+// ln(1 - u53(w0, w1)) of the boost block: the parameter-free part of the boost
+// (the paper's log-uniform buffer)
+template <class Tab = dm::GlobalTables>
+__device__ __forceinline__ double mt_boost_log(uint4 wb, const Tab& tb = Tab()) {
+  return dm::ln_pos(dm::one_minus_u53(wb.x, wb.y), tb);
+}
+template <class Tab = dm::GlobalTables>
+__device__ __forceinline__ double mt_boost_from_log(double L, double g, double alpha,
+                                                    const Tab& tb = Tab()) {
+  return g * dm::exp_nonpos(L / alpha, tb);
 }
 // alpha < 1 boost (R-10): g * exp(ln(1-u53(w0,w1)) / alpha) from block 256 i.
 template <class Tab = dm::GlobalTables>
 __device__ __forceinline__ double mt_boost(uint4 wb, double g, double alpha,
                                            const Tab& tb = Tab()) {
-  return g * dm::exp_nonpos(dm::ln_pos(dm::one_minus_u53(wb.x, wb.y), tb) / alpha, tb);
+  return mt_boost_from_log(mt_boost_log(wb, tb), g, alpha, tb);
 }
 
 // ---- per-sample getters: value of sample i of the bulk call at cursor base --------

@@ -308,3 +308,74 @@ def run_parallel(fn, slices, n_threads):
         t.start()
     for t in ths:
         t.join()
+
+
+# --------------------------------------------------------------------------
+# 8. NEXT row N4: LDA fold-in Gibbs, the paper's LDA use ("sample from
+#    a Dirichlet distribution whose parameters are updated during each
+#    iteration"; footnote: Dirichlet from normalised Gammas) with a fixed
+#    topic-word matrix phi.  Reading R-33, one iteration at
+#    cursor `base`:
+#      n_dk  = #{tokens of doc d with z = k}
+#      theta = Dirichlet(alpha + n_d.) drawn as brng_dirichlet_f64 at `base`
+#              (component (d, k) = Gamma sample d K + k, beta = 1)
+#      u_j   = standard uniform f64 sample j at base + 256 D K
+#      z_j   = first k with fl(u_j C_j) < c_jk, c_jk = fl(c_j,k-1 + fl(theta_dk
+#              phi[w_j, k])), C_j = c_j,K-1 (else the last k with p > 0)
+#    Built from oracle.dirichlet and oracle.std_uniform; the categorical step
+#    is plain Python floats in the stated order.
+# --------------------------------------------------------------------------
+def lda_span(n_docs, k, n_tokens):
+    """Philox blocks one LDA iteration consumes (R-33)."""
+    return GAMMA_STRIDE * n_docs * k + (n_tokens + 1) // 2
+
+
+def lda_counts(doc_off, z, k):
+    """n_dk = #{tokens of doc d assigned topic k} (f64 [D, K])."""
+    D = len(doc_off) - 1
+    n = np.zeros((D, k))
+    for d in range(D):
+        for j in range(int(doc_off[d]), int(doc_off[d + 1])):
+            n[d, int(z[j])] += 1.0
+    return n
+
+
+def lda_categorical(theta_d, phi_w, u):
+    """z for one token: returns (z, x, c) with x = fl(u C) and c the running
+    sums, so a caller can classify a disagreement as a rounding tie."""
+    c = []
+    acc = 0.0
+    last = 0
+    for kk in range(len(theta_d)):
+        p = float(theta_d[kk]) * float(phi_w[kk])
+        acc = acc + p
+        c.append(acc)
+        if p > 0.0:
+            last = kk
+    x = float(u) * acc
+    for kk in range(len(c)):
+        if x < c[kk]:
+            return kk, x, c
+    return last, x, c
+
+
+def lda_iteration(seed, stream, base, doc_off, words, phi, alpha, z):
+    """One fold-in Gibbs iteration (R-33).  phi: [V, K] f64, alpha: [K] f64,
+    z: current topics [T].  Returns dict(z, theta [D, K], trials, x [T],
+    cum (list of running-sum lists per token))."""
+    doc_off = np.asarray(doc_off, np.int64)
+    D, K = len(doc_off) - 1, phi.shape[1]
+    T = int(doc_off[-1])
+    rows = np.asarray(alpha, np.float64)[None, :] + lda_counts(doc_off, z, K)
+    theta, trials, _ = dirichlet(seed, stream, base, rows, dtype=np.float64)
+    u = std_uniform(seed, stream, base + GAMMA_STRIDE * D * K, T, np.float64)
+    z_new = np.empty(T, np.int64)
+    xs = np.empty(T)
+    cums = []
+    for d in range(D):
+        for j in range(int(doc_off[d]), int(doc_off[d + 1])):
+            zz, x, c = lda_categorical(theta[d], phi[int(words[j])], u[j])
+            z_new[j] = zz
+            xs[j] = x
+            cums.append(c)
+    return dict(z=z_new, theta=theta, trials=trials, rows=rows, u=u, x=xs, cum=cums)
