@@ -256,6 +256,46 @@ BRNG_API int brng_gibbs_triangle(brng_t h, uint64_t n_chains, uint64_t n_sweeps,
                         const double* y0, uint64_t burn_in, double* out_x, double* out_y,
                         double* chain_stats, double* final_xy, double* totals);
 
+/* ---- NEXT row N4: LDA fold-in Gibbs consumer (R-33) -------
+ * The paper's motivating use: Gibbs sampling of LDA, which draws a Dirichlet
+ * deviate whose parameters change every iteration.  Fold-in: the
+ * topic-word matrix phi is FIXED (inference of new documents' topics).
+ * Corpus (device pointers only, else BRNG_ERR_PARAM): n_docs documents in CSR
+ * form, doc_off u64[n_docs + 1] (doc_off[0] = 0, non-decreasing,
+ * doc_off[n_docs] = n_tokens), words u32[n_tokens] (< v), phi f64[v][k]
+ * (row w = phi[w, 0..k-1], >= 0), alpha f64[k] (> 0), z u16[n_tokens]
+ * (topics < k; IN: the current state, OUT: the state after n_iter
+ * iterations), theta (nullable) f64[n_docs][k]: theta of the last iteration.
+ * Iteration t at cursor c_t = cursor + t * span, span = 256 n_docs k +
+ * ceil(n_tokens / 2) blocks (the cursor advances by n_iter * span):
+ *   n_dk    = #{tokens j of document d with z_j = k};
+ *   theta_d = Dirichlet(alpha + n_d.) drawn exactly as brng_dirichlet_f64 at
+ *             cursor c_t would (component (d, k) = Gamma sample d k + k);
+ *   u_j     = brng_std_uniform_f64 sample j at cursor c_t + 256 n_docs k;
+ *   z_j     = the first k with fl(u_j C_j) < c_jk, where p_jk =
+ *             fl(theta_dk phi[w_j, k]), c_jk = fl(c_j,k-1 + p_jk) in k order,
+ *             C_j = c_j,k-1 (binary64, no FMA); else the last k with p_jk > 0.
+ * mode: BRNG_LDA_INLINE (the consumer kernel calls the device API getters),
+ * BRNG_LDA_RING (asynchronous service: a producer kernel on a side stream
+ * fills a two-slot ring with iteration t+1's parameter-free standard
+ * deviates -- trial-1 normals, boost log-uniforms, token uniforms -- while the
+ * consumer runs iteration t), BRNG_LDA_BULK (per iteration: counts, the
+ * library's Dirichlet and uniform-fill kernels into scratch, then the
+ * consumer).  All three give the same bits.  Invalid alpha (<= 0 or not
+ * finite) makes the document's theta NaN (counted per component) and its
+ * tokens' z = 0.  k <= BRNG_LDA_MAX_K.  RING/BULK use handle-owned scratch
+ * (two slots of 20 n_docs k + 8 n_tokens bytes / 16 n_docs k + 8 n_tokens),
+ * grown on the first call of a size (not inside a graph capture:
+ * BRNG_ERR_STATE).  Asynchronous on the handle's stream. */
+#define BRNG_LDA_INLINE 0
+#define BRNG_LDA_RING 1
+#define BRNG_LDA_BULK 2
+#define BRNG_LDA_MAX_K 1024u
+BRNG_API int brng_lda_gibbs(brng_t h, uint64_t n_docs, uint32_t k, uint32_t v, uint64_t n_tokens,
+                            const uint64_t* doc_off, const uint32_t* words, const double* phi,
+                            const double* alpha, uint16_t* z, double* theta, uint32_t n_iter,
+                            int mode);
+
 #ifdef __cplusplus
 }
 #endif

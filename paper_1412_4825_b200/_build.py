@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libbrng.so")
-SOURCES = ["brng.cpp", "fill.cu", "gamma.cu", "gibbs.cu"]
+SOURCES = ["brng.cpp", "fill.cu", "gamma.cu", "gibbs.cu", "lda.cu"]
 HEADERS = ["brng_internal.h", "philox.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -58,6 +58,8 @@ _SIGS = {
     "brng_dirichlet_f32": [_H, _vp, _u64, _u64, _vp, _vp],
     "brng_dirichlet_f64": [_H, _vp, _u64, _u64, _vp, _vp],
     "brng_gibbs_triangle": [_H, _u64, _u64, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp],
+    "brng_lda_gibbs": [_H, _u64, C.c_uint32, C.c_uint32, _u64, _vp, _vp, _vp, _vp, _vp, _vp,
+                       C.c_uint32, _int],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -275,3 +277,17 @@ def raw_call(name, *args):
     """Call any exported symbol with raw arguments and return its status
     (used by the error-path tests; no checking)."""
     return getattr(_lib, name)(*args)
+
+
+LDA_INLINE, LDA_RING, LDA_BULK = 0, 1, 2
+LDA_MAX_K = 1024
+
+
+def brng_lda_gibbs(h, n_docs, k, v, n_tokens, doc_off, words, phi, alpha, z, theta=None,
+                   n_iter=1, mode=LDA_INLINE):
+    """LDA fold-in Gibbs (NEXT row N4, include/brng.h): n_iter iterations on
+    device arrays; z (u16) is updated in place."""
+    return _check("brng_lda_gibbs", _lib.brng_lda_gibbs(
+        h, n_docs, k, v, n_tokens, _ptr(doc_off, 8, n_docs + 1), _ptr(words, 4, n_tokens),
+        _ptr(phi, 8, v * k), _ptr(alpha, 8, k), _ptr(z, 2, n_tokens),
+        _ptr(theta, 8, n_docs * k), n_iter, mode))

@@ -66,6 +66,12 @@ struct brng_handle_s {
   // scratch buffers replaced by a larger one stay allocated until
   // brng_destroy: a CUDA graph captured earlier may still reference them
   std::vector<void*> retired;
+  // LDA consumer (NEXT row N4): producer stream, ring / bulk scratch
+  bool lda_ready;
+  cudaStream_t s_prod;
+  cudaEvent_t ev_prod[2], ev_cons[2], ev_lda;
+  void* lda_buf;
+  size_t lda_cap;              // bytes
 };
 
 namespace {
@@ -471,6 +477,7 @@ int brng_create(uint64_t seed, uint64_t stream_id, brng_t* out) {
   h->d_partials = nullptr; h->partials_cap = 0; h->d_totals = nullptr;
   h->d_dir_scratch = nullptr; h->dir_scratch_cap = 0;
   h->pipe_ready = false; h->stage_cap = 0; h->stage_n = 0;
+  h->lda_ready = false; h->lda_buf = nullptr; h->lda_cap = 0;
   if (cudaMalloc(&h->d_err, 2 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMemset(h->d_err, 0, 2 * sizeof(unsigned long long)) != cudaSuccess) {
     delete h;
@@ -495,6 +502,16 @@ int brng_destroy(brng_t h) {
   if (h->d_totals) cudaFree(h->d_totals);
   if (h->d_dir_scratch) cudaFree(h->d_dir_scratch);
   for (void* p : h->retired) cudaFree(p);
+  if (h->lda_buf) cudaFree(h->lda_buf);
+  if (h->lda_ready) {
+    cudaStreamSynchronize(h->s_prod);
+    for (int b = 0; b < 2; ++b) {
+      cudaEventDestroy(h->ev_prod[b]);
+      cudaEventDestroy(h->ev_cons[b]);
+    }
+    cudaEventDestroy(h->ev_lda);
+    cudaStreamDestroy(h->s_prod);
+  }
   if (h->pipe_ready) {
     cudaStreamSynchronize(h->s_in);
     cudaStreamSynchronize(h->s_out);
@@ -707,6 +724,119 @@ int brng_gibbs_triangle(brng_t h, uint64_t n_chains, uint64_t n_sweeps, const do
   }
   if (st) return st;
   commit(h, n_sweeps, 1, 1);
+  return BRNG_OK;
+}
+
+// ---- NEXT row N4: LDA fold-in Gibbs consumer (R-33) --------
+int brng_lda_gibbs(brng_t h, uint64_t n_docs, uint32_t k, uint32_t v, uint64_t n_tokens,
+                   const uint64_t* doc_off, const uint32_t* words, const double* phi,
+                   const double* alpha, uint16_t* z, double* theta, uint32_t n_iter, int mode) {
+  if (!h || !doc_off || !words || !phi || !alpha || !z) return BRNG_ERR_NULL;
+  if (k == 0 || k > BRNG_LDA_MAX_K || v == 0) return BRNG_ERR_SIZE;
+  if (mode < BRNG_LDA_INLINE || mode > BRNG_LDA_BULK) return BRNG_ERR_PARAM;
+  if (n_docs == 0 || n_iter == 0) return BRNG_OK;
+  for (const void* p : {(const void*)doc_off, (const void*)words, (const void*)phi,
+                        (const void*)alpha, (const void*)z, (const void*)theta})
+    if (p && !is_device_ptr(p)) return BRNG_ERR_PARAM;          // device pointers only
+  if (!mul_ok(n_docs, k) || !mul_ok(n_docs * k, BRNG_GAMMA_STRIDE)) return BRNG_ERR_SIZE;
+  const uint64_t dk = n_docs * k;
+  const uint64_t gspan = dk * BRNG_GAMMA_STRIDE;
+  const uint64_t uspan = n_tokens / 2 + (n_tokens % 2);
+  if (gspan > std::numeric_limits<uint64_t>::max() - uspan) return BRNG_ERR_OVERFLOW;
+  const uint64_t span = gspan + uspan;
+  DeviceGuard dg(h);
+  int st = dg.status();
+  if (st) return st;
+  uint64_t base;
+  if ((st = reserve(h, n_iter, 1, span, &base))) return st;
+  Ctx ctx = make_ctx(h);
+  brng::LdaArgs a{};
+  a.n_docs = n_docs; a.n_tokens = n_tokens; a.k = k; a.v = v;
+  a.k0 = ctx.k0; a.k1 = ctx.k1; a.stream = ctx.stream_id;
+  a.doc_off = doc_off; a.words = words; a.phi = phi; a.alpha = alpha; a.z = z;
+  a.work = ctx.work; a.err = ctx.err;
+  // scratch: RING two slots of {z f64, w3 u32, ln(1-u) f64}[dk] + u f64[T];
+  // BULK {alpha + n rows f64, theta f64}[dk] + u f64[T]
+  auto al256 = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t slot = al256(dk * 8) + al256(dk * 4) + al256(dk * 8) + al256(n_tokens * 8);
+  const size_t need = mode == BRNG_LDA_RING ? 2 * slot
+                    : mode == BRNG_LDA_BULK ? al256(dk * 8) * 2 + al256(n_tokens * 8) : 0;
+  if (need > h->lda_cap) {
+    if (capturing(h)) return BRNG_ERR_STATE;
+    if (!grow_scratch(h, &h->lda_buf, &h->lda_cap, need, 1)) return BRNG_ERR_CUDA;
+  }
+  char* buf = static_cast<char*>(h->lda_buf);
+  cudaError_t e = cudaSuccess;
+  if (mode == BRNG_LDA_INLINE) {
+    for (uint32_t t = 0; t < n_iter && e == cudaSuccess; ++t) {
+      a.base = base + (uint64_t)t * span;
+      a.theta_out = t + 1 == n_iter ? theta : nullptr;
+      e = brng::launch_lda_consumer(0, a, ctx);
+    }
+  } else if (mode == BRNG_LDA_BULK) {
+    double* rows = reinterpret_cast<double*>(buf);
+    double* th = reinterpret_cast<double*>(buf + al256(dk * 8));
+    double* ub = reinterpret_cast<double*>(buf + 2 * al256(dk * 8));
+    a.theta_in = th; a.ubuf = ub;
+    for (uint32_t t = 0; t < n_iter && e == cudaSuccess; ++t) {
+      a.base = base + (uint64_t)t * span;
+      a.theta_out = t + 1 == n_iter ? theta : nullptr;
+      e = brng::launch_lda_rows(a, rows, ctx);
+      if (e == cudaSuccess) e = brng::launch_dirichlet(brng::kF64, rows, n_docs, k, th, nullptr,
+                                                       a.base, ctx);
+      if (e == cudaSuccess) e = brng::launch_fill(brng::kStdUniform, brng::kF64, nullptr,
+                                                  nullptr, ub, n_tokens, a.base + gspan, ctx);
+      if (e == cudaSuccess) e = brng::launch_lda_consumer(2, a, ctx);
+    }
+  } else {
+    if (!h->lda_ready) {
+      if (cudaStreamCreateWithFlags(&h->s_prod, cudaStreamNonBlocking) != cudaSuccess)
+        return BRNG_ERR_CUDA;
+      for (int b = 0; b < 2; ++b)
+        if (cudaEventCreateWithFlags(&h->ev_prod[b], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_cons[b], cudaEventDisableTiming) != cudaSuccess)
+          return BRNG_ERR_CUDA;
+      if (cudaEventCreateWithFlags(&h->ev_lda, cudaEventDisableTiming) != cudaSuccess)
+        return BRNG_ERR_CUDA;
+      h->lda_ready = true;
+    }
+    struct Slot { double* zb; uint32_t* w3; double* lb; double* ub; } sl[2];
+    for (int b = 0; b < 2; ++b) {
+      char* p = buf + b * slot;
+      sl[b].zb = reinterpret_cast<double*>(p);
+      sl[b].w3 = reinterpret_cast<uint32_t*>(p + al256(dk * 8));
+      sl[b].lb = reinterpret_cast<double*>(p + al256(dk * 8) + al256(dk * 4));
+      sl[b].ub = reinterpret_cast<double*>(p + al256(dk * 8) + al256(dk * 4) + al256(dk * 8));
+    }
+    // the producer of iteration t + 1 runs on the side stream while the
+    // consumer of iteration t runs on the handle's stream; slot t % 2
+    e = cudaEventRecord(h->ev_lda, h->stream);                     // earlier work first
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->s_prod, h->ev_lda, 0);
+    auto produce = [&](uint32_t t) {
+      brng::LdaArgs pa = a;
+      pa.base = base + (uint64_t)t * span;
+      const Slot& q = sl[t % 2];
+      cudaError_t e2 = cudaSuccess;
+      if (t >= 2) e2 = cudaStreamWaitEvent(h->s_prod, h->ev_cons[t % 2], 0);   // slot free
+      if (e2 == cudaSuccess) e2 = brng::launch_lda_producer(pa, q.zb, q.w3, q.lb, q.ub, ctx,
+                                                            h->s_prod);
+      if (e2 == cudaSuccess) e2 = cudaEventRecord(h->ev_prod[t % 2], h->s_prod);
+      return e2;
+    };
+    if (e == cudaSuccess) e = produce(0);
+    for (uint32_t t = 0; t < n_iter && e == cudaSuccess; ++t) {
+      if (t + 1 < n_iter) e = produce(t + 1);
+      const Slot& q = sl[t % 2];
+      a.base = base + (uint64_t)t * span;
+      a.theta_out = t + 1 == n_iter ? theta : nullptr;
+      a.zbuf = q.zb; a.w3buf = q.w3; a.lbuf = q.lb; a.ubuf = q.ub;
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, h->ev_prod[t % 2], 0);
+      if (e == cudaSuccess) e = brng::launch_lda_consumer(1, a, ctx);
+      if (e == cudaSuccess) e = cudaEventRecord(h->ev_cons[t % 2], h->stream);
+    }
+  }
+  if (e != cudaSuccess) return BRNG_ERR_CUDA;
+  commit(h, n_iter, 1, span);
   return BRNG_OK;
 }
 

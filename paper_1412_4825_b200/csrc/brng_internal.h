@@ -49,4 +49,31 @@ cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
                          double* partials, uint64_t base, const Ctx& ctx,
                          bool accumulate_totals = false);
 
+// NEXT row N4: LDA fold-in Gibbs consumer (lda.cu; reading R-33).
+struct LdaArgs {
+  uint64_t n_docs, n_tokens, base;     // base: cursor of this iteration
+  uint32_t k, v;
+  uint32_t k0, k1;                     // Philox key
+  uint64_t stream;
+  const uint64_t* doc_off;
+  const uint32_t* words;
+  const double* phi;                   // [v][k]
+  const double* alpha;                 // [k]
+  uint16_t* z;                         // [n_tokens], in/out
+  double* theta_out;                   // nullable [n_docs][k]
+  const double* zbuf;                  // RING slot: trial-1 normals [n_docs k]
+  const uint32_t* w3buf;               //            trial-1 words   [n_docs k]
+  const double* lbuf;                  //            boost ln(1-u)   [n_docs k]
+  const double* ubuf;                  // RING / BULK: token uniforms [n_tokens]
+  const double* theta_in;              // BULK: theta [n_docs][k]
+  unsigned long long* work;
+  unsigned long long* err;
+};
+size_t lda_consumer_smem(uint32_t k);
+// src: 0 inline device-API getters, 1 ring slot, 2 bulk buffers
+cudaError_t launch_lda_consumer(int src, const LdaArgs& a, const Ctx& ctx);
+cudaError_t launch_lda_producer(const LdaArgs& a, double* zbuf, uint32_t* w3buf, double* lbuf,
+                                double* ubuf, const Ctx& ctx, cudaStream_t s);
+cudaError_t launch_lda_rows(const LdaArgs& a, double* rows, const Ctx& ctx);
+
 }  // namespace brng

@@ -74,7 +74,7 @@ constexpr int kBoostCap = 64;
 // All 32 lanes must call it (ballots use the full mask).  Every sample's
 // value is a pure function of its counters; the schedule (which lane, which
 // iteration, queued or not) never changes it.
-template <typename Load, typename Sink>
+template <typename P, typename Load, typename Sink>
 __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t base,
                                          const RoundKeys& rk, const Tables& tb, Load load,
                                          Sink sink, uint32_t& nbad, BoostItem* q) {
@@ -83,13 +83,18 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
   uint64_t head = beg + 32;
   uint64_t i = beg + lane;
   bool active = i < end;
-  double alpha = 1.0, beta = 1.0, d = 0.0;
+  // the parameters stay in their storage type until used: a binary32 alpha
+  // converted at the load (the refill, at the end of an iteration) made the
+  // warp wait there for the load (cfg4: 14% of the kernel's stall samples on
+  // that F2F.F64.F32, ncu source view)
+  P alpha_r = P(1), beta_r = P(1);
+  double d = 0.0;
   uint32_t t = 1;
   uint32_t qn = 0;                                   // queued boosts (warp-uniform)
   // issue the parameter loads only; they are consumed after the next trial's
   // Philox block and Box-Muller normal
   auto setup = [&]() {
-    load(i, alpha, beta);
+    load(i, alpha_r, beta_r);
     t = 1;
   };
   // lanes [0, n) take the last n queue entries, boost and sink them
@@ -99,14 +104,15 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
       const BoostItem it = q[qn - n + lane];
       const uint64_t ii = it.i_t & 0x00FFFFFFFFFFFFFFull;
 #if BRNG_SLIM_QUEUE
-      double qa, qb;
+      P qa, qb;
       load(ii, qa, qb);
 #else
       const double qa = it.alpha, qb = it.beta;
 #endif
       const uint4 wb = philox_block_rk(base + (uint64_t)kStride * ii, rk);
-      const double gb = mt_boost(wb, it.g, qa, tb);
-      sink(ii, gb * qb, (uint32_t)(it.i_t >> 56));
+      const double L = brng_dev::mt_boost_log(wb, tb);
+      const double gb = brng_dev::mt_boost_from_log(L, it.g, (double)qa, tb);
+      sink(ii, gb * (double)qb, (uint32_t)(it.i_t >> 56));
     }
     qn -= n;
     __syncwarp();
@@ -115,8 +121,11 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
   while (__any_sync(kFull, active)) {
     bool done = false, boost = false;
     double g = 0.0;
+    double alpha = 1.0;
     if (active) {
       const uint4 w = philox_block_rk(base + (uint64_t)kStride * i + t, rk);
+      alpha = (double)alpha_r;
+      const double beta = (double)beta_r;
       const bool valid = isfinite(alpha) && isfinite(beta) && alpha > 0.0 && beta > 0.0;
       const bool acc = mt_trial(w, alpha, d, g, tb);
       if (!valid) {
@@ -134,7 +143,7 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
       BoostItem it;
       it.g = g;
 #if !BRNG_SLIM_QUEUE
-      it.alpha = alpha; it.beta = beta;
+      it.alpha = alpha; it.beta = (double)beta_r;
 #endif
       it.i_t = i | ((uint64_t)t << 56);
       q[qn + __popc(bm & lt)] = it;
@@ -173,7 +182,7 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
 #ifndef BRNG_INPLACE_MIN
 #define BRNG_INPLACE_MIN 22
 #endif
-constexpr int kRetryCap = 64;
+[[maybe_unused]] constexpr int kRetryCap = 64;
 
 template <typename P, typename Load, typename Sink>
 __device__ __forceinline__ void mt_lockstep(uint64_t beg, uint64_t end, uint64_t base,
@@ -342,11 +351,11 @@ __global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(const 
           be = __ldg(a.beta + i);
         },
 #else
-    mt_queue(
+    mt_queue<T>(
         beg, end, a.base, a.rk, tb,
-        [&](uint64_t i, double& al, double& be) {
-          al = (double)__ldg(a.alpha + i);
-          be = (double)__ldg(a.beta + i);
+        [&](uint64_t i, T& al, T& be) {
+          al = __ldg(a.alpha + i);
+          be = __ldg(a.beta + i);
         },
 #endif
         [&](uint64_t i, double v, uint32_t t) {
@@ -437,11 +446,11 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __gri
           be = T(1);
         },
 #else
-    mt_queue(
+    mt_queue<T>(
         beg, beg + rows * a.k, a.base, a.rk, tb,
-        [&](uint64_t i, double& al, double& be) {
-          al = (double)__ldg(a.alpha + i);
-          be = 1.0;
+        [&](uint64_t i, T& al, T& be) {
+          al = __ldg(a.alpha + i);
+          be = T(1);
         },
 #endif
         [&](uint64_t i, double v, uint32_t t) {
@@ -495,15 +504,15 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(const __gr
   for (uint64_t row = a.scratch ? fetch() : warp; row < a.n_rows;
        row = a.scratch ? fetch() : row + n_warps) {
     const uint64_t beg = row * a.k;
-    auto load = [&](uint64_t i, double& al, double& be) {
-      al = (double)__ldg(a.alpha + i);
-      be = 1.0;
+    auto load = [&](uint64_t i, T& al, T& be) {
+      al = __ldg(a.alpha + i);
+      be = T(1);
     };
     double s = 0.0;
     if (sizeof(T) == 4 && a.scratch) {
       // binary32 with scratch: the warp's own row of binary64 Gammas
       double* g_row = a.scratch + warp * a.k;
-      mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
+      mt_queue<T>(beg, beg + a.k, a.base, a.rk, tb, load,
                [&](uint64_t i, double v, uint32_t t) {
                  g_row[i - beg] = v;
                  if (a.trials) a.trials[i] = (uint8_t)t;
@@ -518,7 +527,7 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(const __gr
       for (uint64_t j = lane; j < a.k; j += 32) a.out[beg + j] = (T)(g_row[j] * inv);
       __syncwarp();
     } else if constexpr (sizeof(T) == 8) {
-      mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
+      mt_queue<T>(beg, beg + a.k, a.base, a.rk, tb, load,
                [&](uint64_t i, double v, uint32_t t) {
                  a.out[i] = (T)v;
                  if (a.trials) a.trials[i] = (uint8_t)t;
@@ -531,11 +540,11 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(const __gr
       const double inv = 1.0 / s;
       for (uint64_t j = lane; j < a.k; j += 32) a.out[beg + j] = (T)((double)a.out[beg + j] * inv);
     } else {
-      mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
+      mt_queue<T>(beg, beg + a.k, a.base, a.rk, tb, load,
                [&](uint64_t, double v, uint32_t) { s += v; }, nbad, q);
       s = warp_sum(s);
       const double inv = 1.0 / s;
-      mt_queue(beg, beg + a.k, a.base, a.rk, tb, load,
+      mt_queue<T>(beg, beg + a.k, a.base, a.rk, tb, load,
                [&](uint64_t i, double v, uint32_t t) {
                  a.out[i] = (T)(v * inv);
                  if (a.trials) a.trials[i] = (uint8_t)t;

@@ -110,4 +110,12 @@ cudaError_t launch_gibbs(uint64_t n_chains, uint64_t n_sweeps, const double* x0,
   return cudaSuccess;
 }
 
+size_t lda_consumer_smem(uint32_t k) { return (size_t)4 * k * 12; }
+cudaError_t launch_lda_consumer(int, const LdaArgs&, const Ctx&) { return cudaSuccess; }
+cudaError_t launch_lda_producer(const LdaArgs&, double*, uint32_t*, double*, double*, const Ctx&,
+                                cudaStream_t) {
+  return cudaSuccess;
+}
+cudaError_t launch_lda_rows(const LdaArgs&, double*, const Ctx&) { return cudaSuccess; }
+
 }  // namespace brng

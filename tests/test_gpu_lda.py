@@ -1,0 +1,122 @@
+"""NEXT row N4 on the GPU: the LDA fold-in Gibbs consumer (brng_lda_gibbs,
+include/brng.h; reading R-33).
+
+- chained one-iteration parity against the oracle-side loop built from
+  oracle.dirichlet (oracle.lda_iteration): from the same state z, theta within
+  the Dirichlet parity tolerance and every token's topic equal, except
+  rounding ties of the categorical step (x within 1e-9 C of the boundary),
+  which are counted;
+- the three deviate sources (inline device API, asynchronous producer ring,
+  synchronous bulk calls) give the same bits over several iterations, and
+  the cursor advances by n_iter * (256 D K + ceil(T/2));
+- the inline theta equals brng_dirichlet_f64 at the same cursor bit for bit;
+- argument errors.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads
+from tests import parity
+from tests.gpu_util import dev, handle
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+import paper_1412_4825_b200 as B  # noqa: E402
+
+
+def _corpus(D=300, K=16, V=64, L=30, seed=5):
+    c = workloads.lda_corpus(D, K, V, L, seed=seed)
+    alpha = torch.linspace(0.05, 1.5, K, dtype=torch.float64)     # boosted and not
+    return c, alpha
+
+
+def _run(c, alpha, z, n_iter, mode, seed=77, stream=3, cursor=0, theta=True):
+    D, K = len(c["doc_off"]) - 1, c["phi"].shape[1]
+    V, T = c["phi"].shape[0], c["n_tokens"]
+    zd = z.to(dev()).clone()
+    th = torch.empty(D, K, dtype=torch.float64, device=dev()) if theta else None
+    with handle(seed, stream, cursor) as h:
+        B.brng_lda_gibbs(h, D, K, V, T, c["doc_off"].to(dev()), c["words"].to(dev()),
+                         c["phi"].to(dev()), alpha.to(dev()), zd, th, n_iter, mode)
+        end = B.brng_get_offset(h)
+        errs = B.brng_device_errors(h)
+    return zd.cpu().numpy().astype(np.int64), (th.cpu().numpy() if theta else None), end, errs
+
+
+def test_chained_iterations_match_oracle():
+    c, alpha = _corpus()
+    D, K, T = len(c["doc_off"]) - 1, c["phi"].shape[1], c["n_tokens"]
+    doc_off, words = c["doc_off"].numpy(), c["words"].numpy()
+    phi, al = c["phi"].numpy(), alpha.numpy()
+    z = c["z0"]
+    cursor = (1 << 32) - 5000                       # the iterations cross a 2^32 block boundary
+    span = oracle.lda_span(D, K, T)
+    n_tie = 0
+    for it in range(4):
+        zg, thg, end, errs = _run(c, alpha, z, 1, B.LDA_INLINE, cursor=cursor)
+        assert end == cursor + span and errs == 0
+        r = oracle.lda_iteration(77, 3, cursor, doc_off, words, phi, al,
+                                 z.numpy().astype(np.int64))
+        # theta: the Dirichlet criterion (tests/parity.py), rows as in brng_dirichlet_f64
+        dr = parity.value_check(thg.reshape(-1), r["theta"].reshape(-1),
+                                np.abs(r["theta"].reshape(-1)), np.float64,
+                                lambda j: parity.gamma_condition(77, 3, cursor, j,
+                                                                 float(r["rows"].reshape(-1)[j]),
+                                                                 int(r["trials"].reshape(-1)[j])),
+                                f"theta it{it}")
+        assert dr["ratio"] <= 1.0
+        for j in np.flatnonzero(zg != r["z"]):
+            # a disagreement must be a rounding tie of x against a running sum
+            cum, x = np.array(r["cum"][j]), r["x"][j]
+            kk = min(int(zg[j]), int(r["z"][j]))
+            assert abs(x - cum[kk]) <= 1e-9 * cum[-1], (it, j, zg[j], r["z"][j])
+            n_tie += 1
+        z = torch.from_numpy(zg.astype(np.int16))   # continue from the GPU's state
+        cursor += span
+    assert n_tie <= 2
+
+
+def test_three_sources_bit_identical():
+    c, alpha = _corpus(D=517, K=40, V=200, L=45, seed=9)
+    D, K, T = len(c["doc_off"]) - 1, c["phi"].shape[1], c["n_tokens"]
+    res = [_run(c, alpha, c["z0"], 3, m, cursor=123) for m in (B.LDA_INLINE, B.LDA_RING,
+                                                               B.LDA_BULK)]
+    for zg, th, end, errs in res[1:]:
+        assert np.array_equal(zg, res[0][0]) and np.array_equal(th, res[0][1])
+        assert end == res[0][2] == 123 + 3 * oracle.lda_span(D, K, T) and errs == 0
+    # the state moved (the sampler is not a no-op) and stays in range
+    assert (res[0][0] != c["z0"].numpy()).mean() > 0.3 and res[0][0].max() < K
+
+
+def test_inline_theta_equals_bulk_dirichlet_call():
+    c, alpha = _corpus(D=200, K=24, V=50, L=20, seed=11)
+    D, K = len(c["doc_off"]) - 1, c["phi"].shape[1]
+    zg, th, _, _ = _run(c, alpha, c["z0"], 1, B.LDA_INLINE, cursor=999)
+    rows = torch.from_numpy(alpha.numpy()[None, :] +
+                            oracle.lda_counts(c["doc_off"].numpy(), c["z0"].numpy().astype(np.int64),
+                                              K)).to(dev())
+    out = torch.empty(D, K, dtype=torch.float64, device=dev())
+    with handle(77, 3, 999) as h:
+        B.brng_dirichlet_f64(h, rows, D, K, out, None)
+    assert np.array_equal(out.cpu().numpy(), th)
+
+
+def test_lda_argument_errors():
+    c, alpha = _corpus(D=8, K=4, V=8, L=5)
+    D, K, V, T = 8, 4, 8, c["n_tokens"]
+    d = {k: v.to(dev()) for k, v in c.items() if k != "n_tokens"}
+    with handle(1) as h:
+        raw = lambda *a: B.brng._lib.brng_lda_gibbs(h, *a)  # noqa: E731
+        args = [D, K, V, T, d["doc_off"].data_ptr(), d["words"].data_ptr(), d["phi"].data_ptr(),
+                alpha.to(dev()).data_ptr(), d["z0"].data_ptr(), None, 1]
+        assert raw(*args[:1], 0, *args[2:], 0) == -2                 # k == 0
+        assert raw(*args, 7) == -4                                   # unknown mode
+        host_z = c["z0"].clone()
+        a2 = list(args); a2[8] = host_z.data_ptr()
+        assert raw(*a2, 0) == -4                                     # host pointer
+        assert B.brng_get_offset(h) == 0
+        assert raw(*args[:-1], 0, 0) == 0 and B.brng_get_offset(h) == 0   # n_iter == 0

@@ -79,3 +79,38 @@ def cfg4_params(n_docs: int, k: int = 256, seed: int = 3, device="cpu",
     n = torch.poisson(rate, generator=g)
     alpha = 0.1 + torch.where(support, n, torch.zeros_like(n)).to(torch.float64)
     return alpha.to(dtype)
+
+
+# NEXT row N4 (reading R-33): a synthetic LDA fold-in corpus.  Documents'
+# lengths ~ 1 + Poisson(mean_len - 1); each document mixes a few topics of a
+# fixed topic-word matrix phi (topic rows ~ Dirichlet(beta) over the
+# vocabulary, drawn with torch's own generator); initial topics uniform.
+LDA = dict(name="lda_foldin_100k_docs_K64", seed=5, n_docs=100_000, k=64, v=20_000,
+           mean_len=150, alpha=0.1, beta=0.05)
+
+
+def lda_corpus(n_docs: int, k: int, v: int, mean_len: float, seed: int = 5,
+               beta: float = 0.05, device="cpu"):
+    """dict(doc_off u64 [D+1], words u32 [T], phi f64 [V, K], z0 u16 [T], n_tokens)."""
+    g = _gen(seed, "cpu")
+    lens = 1 + torch.poisson(torch.full((n_docs,), float(mean_len - 1)), generator=g).long()
+    doc_off = torch.zeros(n_docs + 1, dtype=torch.int64)
+    doc_off[1:] = torch.cumsum(lens, 0)
+    T = int(doc_off[-1])
+    gam = torch._standard_gamma(torch.full((k, v), float(beta), dtype=torch.float64),
+                                generator=g)
+    phi_kv = gam / gam.sum(dim=1, keepdim=True)
+    # each document draws its words from 3 of the topics (LDA-shaped corpus)
+    doc_topics = torch.randint(0, k, (n_docs, 3), generator=g)
+    tok_doc = torch.repeat_interleave(torch.arange(n_docs), lens)
+    pick = doc_topics[tok_doc, torch.randint(0, 3, (T,), generator=g)]
+    words = torch.empty(T, dtype=torch.int64)
+    for t in range(k):
+        sel = (pick == t).nonzero().squeeze(1)
+        if sel.numel():
+            words[sel] = torch.multinomial(phi_kv[t], sel.numel(), replacement=True, generator=g)
+    z0 = torch.randint(0, k, (T,), generator=g)
+    # int64 / int32 / int16 carry the u64 / u32 / u16 bits the C ABI reads
+    return dict(doc_off=doc_off.to(device), words=words.to(torch.int32).to(device),
+                phi=phi_kv.t().contiguous().to(device), z0=z0.to(torch.int16).to(device),
+                n_tokens=T)
