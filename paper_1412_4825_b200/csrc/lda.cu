@@ -28,6 +28,8 @@
 //   BULK    synchronous batch calls per iteration: counts -> alpha + n rows,
 //           the library's Dirichlet kernel, the library's uniform fill, then
 //           the consumer reads theta and u from HBM.
+#include <algorithm>
+
 #include "brng_internal.h"
 #include "philox.cuh"
 
@@ -219,12 +221,23 @@ cudaError_t launch_lda_consumer(int src, const LdaArgs& a, const Ctx& ctx) {
   cudaError_t e = cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), ctx.stream);
   if (e != cudaSuccess) return e;
   const uint64_t want = (a.n_docs + 3) / 4;
+  // The categorical step reads the token's phi row twice (total, then
+  // search): the second read should hit L1.  Left to itself the driver gives
+  // a low-register consumer (BULK: 31 registers) a shared-memory carve-out
+  // for 16 CTAs/SM, which leaves little L1 (K = 256: 5.4 vs 3.0 ms per
+  // iteration); every consumer gets the carve-out for kLdaCtasPerSm CTAs.
+  constexpr int kLdaCtasPerSm = 8;
+  const int carve = (int)std::min<size_t>(
+      100, (kLdaCtasPerSm * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) {
       cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem);
       if (e2 != cudaSuccess) return e2;
     }
+    cudaError_t e3 = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          carve);
+    if (e3 != cudaSuccess) return e3;
     const uint64_t cap = (uint64_t)ctas_for(kern, smem, ctx.num_sms);
     const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
     kern<<<g, kLdaThreads, smem, ctx.stream>>>(a);
