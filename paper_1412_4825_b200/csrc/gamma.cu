@@ -32,6 +32,9 @@ constexpr int kThreads = 256;
 #define BRNG_GAMMA_CHUNK 2048
 #endif
 constexpr uint64_t kChunk = BRNG_GAMMA_CHUNK;
+#ifndef BRNG_GAMMA_SPEC
+#define BRNG_GAMMA_SPEC 0     // speculative boosts for Gamma (cfg3: 36% boosted)
+#endif
 constexpr uint32_t kStride = 256;          // blocks per sample (R-11)
 constexpr uint32_t kMaxTrial = 255;
 constexpr uint32_t kFull = 0xffffffffu;
@@ -74,7 +77,12 @@ constexpr int kBoostCap = 64;
 // All 32 lanes must call it (ballots use the full mask).  Every sample's
 // value is a pure function of its counters; the schedule (which lane, which
 // iteration, queued or not) never changes it.
-template <typename P, typename Load, typename Sink>
+// SPEC (speculative boost): every sample's boost log-uniform ln(1-u) is
+// computed with its first trial (a second, independent Philox chain in the
+// same lane: ILP) and kept in a register, and an accepted alpha<1 sample is
+// boosted in place -- no boost queue.  Pays when most samples are boosted
+// (cfg4: 91%); a sample with alpha >= 1 wastes the block.
+template <typename P, bool SPEC = false, typename Load, typename Sink>
 __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t base,
                                          const RoundKeys& rk, const Tables& tb, Load load,
                                          Sink sink, uint32_t& nbad, BoostItem* q) {
@@ -89,6 +97,7 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
   // that F2F.F64.F32, ncu source view)
   P alpha_r = P(1), beta_r = P(1);
   double d = 0.0;
+  double Lb = 0.0;                                   // SPEC: boost ln(1-u) of the lane's sample
   uint32_t t = 1;
   uint32_t qn = 0;                                   // queued boosts (warp-uniform)
   // issue the parameter loads only; they are consumed after the next trial's
@@ -123,7 +132,9 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
     double g = 0.0;
     double alpha = 1.0;
     if (active) {
-      const uint4 w = philox_block_rk(base + (uint64_t)kStride * i + t, rk);
+      const uint64_t pos = base + (uint64_t)kStride * i;
+      const uint4 w = philox_block_rk(pos + t, rk);
+      if (SPEC && t == 1) Lb = brng_dev::mt_boost_log(philox_block_rk(pos, rk), tb);
       alpha = (double)alpha_r;
       const double beta = (double)beta_r;
       const bool valid = isfinite(alpha) && isfinite(beta) && alpha > 0.0 && beta > 0.0;
@@ -136,9 +147,15 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
         done = true; t = 0; ++nbad;
       }
       boost = done && t != 0 && alpha < 1.0;
-      if (done && !boost) sink(i, t != 0 ? g * beta : qnan(), t);
+      if (SPEC) {
+        if (boost) g = brng_dev::mt_boost_from_log(Lb, g, alpha, tb);
+        if (done) sink(i, t != 0 ? g * beta : qnan(), t);
+        boost = false;
+      } else if (done && !boost) {
+        sink(i, t != 0 ? g * beta : qnan(), t);
+      }
     }
-    const uint32_t bm = __ballot_sync(kFull, boost);
+    const uint32_t bm = SPEC ? 0u : __ballot_sync(kFull, boost);
     if (boost) {
       BoostItem it;
       it.g = g;
@@ -149,7 +166,7 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
       q[qn + __popc(bm & lt)] = it;
     }
     qn += __popc(bm);
-    if (qn >= 32) drain(32);
+    if (!SPEC && qn >= 32) drain(32);
     const uint32_t dm = __ballot_sync(kFull, done);
     if (done) {
       i = head + __popc(dm & lt);
@@ -158,7 +175,7 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
     }
     head += __popc(dm);
   }
-  if (qn) drain(qn);
+  if (!SPEC && qn) drain(qn);
 }
 
 // ---- lockstep schedule (BRNG_LOCKSTEP) ---------------------------------------
@@ -351,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(const 
           be = __ldg(a.beta + i);
         },
 #else
-    mt_queue<T>(
+    mt_queue<T, BRNG_GAMMA_SPEC != 0>(
         beg, end, a.base, a.rk, tb,
         [&](uint64_t i, T& al, T& be) {
           al = __ldg(a.alpha + i);
@@ -385,6 +402,9 @@ struct DirArgs {
 };
 
 constexpr int kDirThreads = 128;     // 4 warps / CTA, one row per warp
+#ifndef BRNG_DIR_SPEC
+#define BRNG_DIR_SPEC 1                  // speculative in-place boosts (mt_queue SPEC)
+#endif
 #ifndef BRNG_DIR_SMEM_K
 #define BRNG_DIR_SMEM_K 2048
 #endif
@@ -446,7 +466,7 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __gri
           be = T(1);
         },
 #else
-    mt_queue<T>(
+    mt_queue<T, BRNG_DIR_SPEC != 0>(
         beg, beg + rows * a.k, a.base, a.rk, tb,
         [&](uint64_t i, T& al, T& be) {
           al = __ldg(a.alpha + i);
