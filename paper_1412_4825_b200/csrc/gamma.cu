@@ -134,7 +134,12 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
     if (active) {
       const uint64_t pos = base + (uint64_t)kStride * i;
       const uint4 w = philox_block_rk(pos + t, rk);
-      if (SPEC && t == 1) Lb = brng_dev::mt_boost_log(philox_block_rk(pos, rk), tb);
+      if (SPEC) {
+        // every lane computes it, kept from trial 1: no divergent region
+        // (retrying lanes would idle through it anyway): cfg4 4.160 -> 4.052 ms
+        const double Ln = brng_dev::mt_boost_log(philox_block_rk(pos, rk), tb);
+        Lb = t == 1 ? Ln : Lb;
+      }
       alpha = (double)alpha_r;
       const double beta = (double)beta_r;
       const bool valid = isfinite(alpha) && isfinite(beta) && alpha > 0.0 && beta > 0.0;
@@ -148,7 +153,8 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
       }
       boost = done && t != 0 && alpha < 1.0;
       if (SPEC) {
-        if (boost) g = brng_dev::mt_boost_from_log(Lb, g, alpha, tb);
+        const double gb = brng_dev::mt_boost_from_log(Lb, g, alpha, tb);
+        g = boost ? gb : g;
         if (done) sink(i, t != 0 ? g * beta : qnan(), t);
         boost = false;
       } else if (done && !boost) {

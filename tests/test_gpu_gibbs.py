@@ -155,6 +155,35 @@ def test_cfg5_full_size():
     assert_ks_uniform(2 * fxv - fxv * fxv, "cfg5 final-x marginal")
 
 
+@pytest.mark.slow
+def test_cfg5_strong_scaling_shard_full_size():
+    """The bench's N = 8 launch configuration (bench.py --scaling strong): rank
+    7's shard of cfg5, 2^21 chains from stream 7 * 2^21, 4096 sweeps -- 9.22
+    resident waves, i.e. full rounds plus one-chain tail rounds.  Sampled
+    chains (incl. both ends and the tail rounds) bit-exact against the oracle,
+    histogram complete, transient-exact pooled means."""
+    from paper_1412_4825_b200 import shard as S
+    c = workloads.CFG5
+    lo, hi = S.shard_range(c["n_chains"], 7, 8)
+    nc, ns = hi - lo, c["n_sweeps"]
+    g = _run(c["seed"], S.gibbs_stream(0, lo), 0, nc, ns, samples=False)
+    tot = g["totals"]
+    assert g["n_invalid"] == 0 and tot[8] == nc and tot[HDR:].sum() == nc * ns
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    wave = 2 * 256 * 3 * sms
+    tail0 = (nc // wave) * wave                       # first chain of the tail rounds
+    rng = np.random.default_rng(8)
+    picks = np.concatenate([[0, 1, tail0 - 1, tail0, tail0 + 1, nc - 1],
+                            rng.integers(0, nc, 60), rng.integers(tail0, nc, 30)])
+    for cidx in picks:
+        r = oracle.gibbs_triangle(c["seed"], lo + int(cidx), 0, 1, ns, want_samples=False)
+        assert np.array_equal(g["chain_stats"][:, cidx], r["chain_stats"][:, 0]), cidx
+        assert np.array_equal(g["final_xy"][:, cidx], r["final_xy"][:, 0]), cidx
+    ex = 1 / 3 - (1 - 4.0**-ns) / (9 * ns)
+    sd = math.sqrt((5 / 3) * (1 / 18) / ns / nc)
+    assert abs(tot[0] / nc - ex) < 6 * sd
+
+
 def test_host_pipeline_multi_chunk_gibbs():
     nc, ns = 3_000_017, 16                            # chain_stats 120 MB -> 2 chunks
     g = _run(42, 0, 0, nc, ns, samples=False)
