@@ -11,6 +11,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "../../include/brng.h"
 
 size_t fake_cuda_live_allocs();
@@ -168,8 +170,45 @@ static void gibbs_host() {
   CHECK(brng_destroy(h) == BRNG_OK);
 }
 
+// LDA consumer entry point (N4): argument checks, device-pointer rule,
+// cursor span, RING / BULK scratch growth and release
+static void lda() {
+  brng_t h;
+  CHECK(brng_create(5, 0, &h) == BRNG_OK);
+  const uint64_t D = 50, T = 777;
+  const uint32_t K = 16, V = 30;
+  void *off, *w, *phi, *al, *z, *th;
+  CHECK(cudaMalloc(&off, (D + 1) * 8) == cudaSuccess && cudaMalloc(&w, T * 4) == cudaSuccess);
+  CHECK(cudaMalloc(&phi, V * K * 8) == cudaSuccess && cudaMalloc(&al, K * 8) == cudaSuccess);
+  CHECK(cudaMalloc(&z, T * 2) == cudaSuccess && cudaMalloc(&th, D * K * 8) == cudaSuccess);
+  auto off_p = static_cast<const uint64_t*>(off);
+  auto w_p = static_cast<const uint32_t*>(w);
+  auto phi_p = static_cast<const double*>(phi);
+  auto al_p = static_cast<const double*>(al);
+  auto z_p = static_cast<uint16_t*>(z);
+  auto th_p = static_cast<double*>(th);
+  std::vector<uint16_t> host_z(T);
+  CHECK(brng_lda_gibbs(h, D, 0, V, T, off_p, w_p, phi_p, al_p, z_p, th_p, 1, 0) == BRNG_ERR_SIZE);
+  CHECK(brng_lda_gibbs(h, D, BRNG_LDA_MAX_K + 1, V, T, off_p, w_p, phi_p, al_p, z_p, th_p, 1, 0) ==
+        BRNG_ERR_SIZE);
+  CHECK(brng_lda_gibbs(h, D, K, V, T, off_p, w_p, phi_p, al_p, z_p, th_p, 1, 9) == BRNG_ERR_PARAM);
+  CHECK(brng_lda_gibbs(h, D, K, V, T, off_p, w_p, phi_p, al_p, host_z.data(), th_p, 1, 0) ==
+        BRNG_ERR_PARAM);
+  CHECK(brng_lda_gibbs(h, D, K, V, T, nullptr, w_p, phi_p, al_p, z_p, th_p, 1, 0) == BRNG_ERR_NULL);
+  uint64_t c = 0;
+  CHECK(brng_get_offset(h, &c) == BRNG_OK && c == 0);
+  const uint64_t span = 256ull * D * K + (T + 1) / 2;
+  for (int mode : {BRNG_LDA_INLINE, BRNG_LDA_RING, BRNG_LDA_BULK, BRNG_LDA_RING})
+    CHECK(brng_lda_gibbs(h, D, K, V, T, off_p, w_p, phi_p, al_p, z_p, th_p, 3, mode) == BRNG_OK);
+  CHECK(brng_get_offset(h, &c) == BRNG_OK && c == 4 * 3 * span);
+  CHECK(brng_lda_gibbs(h, D, K, V, T, off_p, w_p, phi_p, al_p, z_p, nullptr, 0, 0) == BRNG_OK);
+  CHECK(brng_destroy(h) == BRNG_OK);
+  for (void* p : {off, w, phi, al, z, th}) cudaFree(p);
+}
+
 int main() {
   errors();
+  lda();
   fills_host();
   gamma_dirichlet_host();
   gibbs_host();
