@@ -79,20 +79,32 @@ GAMMA_SAMPLE_SLOTS = 1
 DIRICHLET_SAMPLE_SLOTS = 2
 
 
-def ncu_traffic(kernel_substr):
-    """DRAM bytes (read + write) per launch of a kernel from the committed ncu
-    --set full summary (profiles/*_ncu.json, tools/ncu_summary.py), or None."""
+def _ncu_entry(kernel_substr):
+    """The newest committed ncu --set full summary (profiles/*_ncu.json,
+    tools/ncu_summary.py) entry of a kernel: the full-size launch, i.e. the
+    longest capture of that kernel in the newest file that has one (a file
+    may also hold a smaller launch of the same kernel, e.g. a strong-scaling
+    shard)."""
     import glob
     best = None
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu.json"))):
         try:
             with open(path) as f:
-                for k in json.load(f)["kernels"]:
-                    if kernel_substr in k.get("kernel", "") and "traffic_GB" in k:
-                        best = (k["traffic_GB"] * 1e9, os.path.basename(path))
+                ks = [k for k in json.load(f)["kernels"] if kernel_substr in k.get("kernel", "")]
         except Exception:
             continue
+        if ks:
+            best = (max(ks, key=lambda k: k.get("time_ms", 0.0)), os.path.basename(path))
     return best
+
+
+def ncu_traffic(kernel_substr):
+    """DRAM bytes (read + write) per launch of a kernel from the committed ncu
+    summary, or None."""
+    e = _ncu_entry(kernel_substr)
+    if e is None or "traffic_GB" not in e[0]:
+        return None
+    return e[0]["traffic_GB"] * 1e9, e[1]
 
 
 NCU_KERNEL = {"cfg1_gibbs": "gibbs_lat_kernel<1>", "cfg2_gaussian": "fill_kernel<float, 3, 0>",
@@ -104,18 +116,12 @@ NCU_KERNEL = {"cfg1_gibbs": "gibbs_lat_kernel<1>", "cfg2_gaussian": "fill_kernel
 def ncu_evidence(kernel_substr):
     """Pipe / issue / DRAM utilisation of a kernel from the committed ncu
     summary (profiles/*_ncu.json), labelled with its file; {} if absent."""
-    import glob
-    ev = {}
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu.json"))):
-        try:
-            with open(path) as f:
-                for k in json.load(f)["kernels"]:
-                    if kernel_substr in k.get("kernel", ""):
-                        ev = {m: k[m] for m in ("issue_active_pct", "fmaheavy_pct", "alu_pct",
-                                                "dram_pct_peak", "warps_active_pct") if m in k}
-                        ev["source"] = os.path.basename(path)
-        except Exception:
-            continue
+    e = _ncu_entry(kernel_substr)
+    if e is None:
+        return {}
+    ev = {m: e[0][m] for m in ("issue_active_pct", "fmaheavy_pct", "alu_pct", "dram_pct_peak",
+                               "warps_active_pct") if m in e[0]}
+    ev["source"] = e[1]
     return ev
 
 
