@@ -213,6 +213,7 @@ BRNG_API int brng_gamma_f64(brng_t h, const double* alpha, const double* beta, d
  * i = r*k + j of the contract above with beta = 1; S_r = sum_j y_rj (binary64,
  * any order); out[r][j] = y_rj / S_r rounded to the output type.  An invalid
  * component makes its whole row NaN.  trials: nullable u8[n_rows][k].
+ * 1 <= k < 2^24 (BRNG_ERR_SIZE otherwise).
  * Arithmetic: the kernels form fl(1/S_r) once per row and output
  * y_rj * fl(1/S_r) (binary64) rounded to the output type; this is within one
  * binary64 ulp of y_rj / S_r before that rounding, inside the parity

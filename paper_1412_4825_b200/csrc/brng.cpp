@@ -412,7 +412,7 @@ int gamma_common(brng_t h, int dtype, const void* alpha, const void* beta, void*
 int dirichlet_common(brng_t h, int dtype, const void* alpha, uint64_t n_rows, uint64_t k,
                      void* out, uint8_t* trials, size_t esize) {
   if (!h || !alpha || !out) return BRNG_ERR_NULL;
-  if (k == 0) return BRNG_ERR_SIZE;
+  if (k == 0 || k >= (1ull << 24)) return BRNG_ERR_SIZE;   // the kernels' 24-bit row offsets
   if (n_rows == 0) return BRNG_OK;
   if (!mul_ok(n_rows, k)) return BRNG_ERR_SIZE;
   const uint64_t n = n_rows * k;

@@ -66,14 +66,20 @@ struct BoostItem {
 #if !BRNG_SLIM_QUEUE
   double alpha, beta;
 #endif
-  uint64_t i_t;            // sample index | trial << 56
+  uint32_t off_t;          // sample offset in the queue's range | trial << 24
+  uint32_t pad;
 };
 constexpr int kBoostCap = 64;
+// a queue's range of samples is < 2^24 (Gamma chunks of kChunk, Dirichlet
+// row groups / rows: the host limits k < 2^24), so 32-bit offsets suffice
+constexpr uint32_t kOffBits = 24;
 
-// Warp-cooperative Gamma queue over sample indices [beg, end).
-//   load(i, alpha, beta)  -- parameters of sample i
-//   sink(i, value, trial) -- value = g * beta (NaN when invalid / capped)
-//   q                     -- this warp's BoostItem[kBoostCap] in shared memory
+// Warp-cooperative Gamma queue over the samples beg + [0, n), n < 2^24.
+//   load(off, alpha, beta)  -- parameters of sample beg + off
+//   sink(off, value, trial) -- value = g * beta (NaN when invalid / capped)
+//   q                       -- this warp's BoostItem[kBoostCap] in shared memory
+// Offsets are 32-bit (the callers' lambdas address arrays already shifted by
+// beg): the per-iteration bookkeeping has no 64-bit index arithmetic.
 // All 32 lanes must call it (ballots use the full mask).  Every sample's
 // value is a pure function of its counters; the schedule (which lane, which
 // iteration, queued or not) never changes it.
@@ -83,14 +89,15 @@ constexpr int kBoostCap = 64;
 // boosted in place -- no boost queue.  Pays when most samples are boosted
 // (cfg4: 91%); a sample with alpha >= 1 wastes the block.
 template <typename P, bool SPEC = false, typename Load, typename Sink>
-__device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t base,
+__device__ __forceinline__ void mt_queue(uint64_t beg, uint32_t n, uint64_t base,
                                          const RoundKeys& rk, const Tables& tb, Load load,
                                          Sink sink, uint32_t& nbad, BoostItem* q) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
-  uint64_t head = beg + 32;
-  uint64_t i = beg + lane;
-  bool active = i < end;
+  const uint64_t base_c = base + (uint64_t)kStride * beg;   // block of sample beg
+  uint32_t head = 32;
+  uint32_t off = lane;
+  bool active = off < n;
   // the parameters stay in their storage type until used: a binary32 alpha
   // converted at the load (the refill, at the end of an iteration) made the
   // warp wait there for the load (cfg4: 14% of the kernel's stall samples on
@@ -103,27 +110,27 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
   // issue the parameter loads only; they are consumed after the next trial's
   // Philox block and Box-Muller normal
   auto setup = [&]() {
-    load(i, alpha_r, beta_r);
+    load(off, alpha_r, beta_r);
     t = 1;
   };
-  // lanes [0, n) take the last n queue entries, boost and sink them
-  auto drain = [&](uint32_t n) {
+  // lanes [0, k) take the last k queue entries, boost and sink them
+  auto drain = [&](uint32_t k) {
     __syncwarp();
-    if (lane < n) {
-      const BoostItem it = q[qn - n + lane];
-      const uint64_t ii = it.i_t & 0x00FFFFFFFFFFFFFFull;
+    if (lane < k) {
+      const BoostItem it = q[qn - k + lane];
+      const uint32_t oo = it.off_t & ((1u << kOffBits) - 1);
 #if BRNG_SLIM_QUEUE
       P qa, qb;
-      load(ii, qa, qb);
+      load(oo, qa, qb);
 #else
       const double qa = it.alpha, qb = it.beta;
 #endif
-      const uint4 wb = philox_block_rk(base + (uint64_t)kStride * ii, rk);
+      const uint4 wb = philox_block_rk(base_c + ((uint64_t)oo << 8), rk);
       const double L = brng_dev::mt_boost_log(wb, tb);
       const double gb = brng_dev::mt_boost_from_log(L, it.g, (double)qa, tb);
-      sink(ii, gb * (double)qb, (uint32_t)(it.i_t >> 56));
+      sink(oo, gb * (double)qb, it.off_t >> kOffBits);
     }
-    qn -= n;
+    qn -= k;
     __syncwarp();
   };
   if (active) setup();
@@ -132,7 +139,7 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
     double g = 0.0;
     double alpha = 1.0;
     if (active) {
-      const uint64_t pos = base + (uint64_t)kStride * i;
+      const uint64_t pos = base_c + ((uint64_t)off << 8);   // kStride = 256 blocks per sample
       const uint4 w = philox_block_rk(pos + t, rk);
       if (SPEC) {
         // every lane computes it, kept from trial 1: no divergent region
@@ -155,10 +162,10 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
       if (SPEC) {
         const double gb = brng_dev::mt_boost_from_log(Lb, g, alpha, tb);
         g = boost ? gb : g;
-        if (done) sink(i, t != 0 ? g * beta : qnan(), t);
+        if (done) sink(off, t != 0 ? g * beta : qnan(), t);
         boost = false;
       } else if (done && !boost) {
-        sink(i, t != 0 ? g * beta : qnan(), t);
+        sink(off, t != 0 ? g * beta : qnan(), t);
       }
     }
     const uint32_t bm = SPEC ? 0u : __ballot_sync(kFull, boost);
@@ -168,157 +175,20 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint64_t end, uint64_t ba
 #if !BRNG_SLIM_QUEUE
       it.alpha = alpha; it.beta = (double)beta_r;
 #endif
-      it.i_t = i | ((uint64_t)t << 56);
+      it.off_t = off | (t << kOffBits);
       q[qn + __popc(bm & lt)] = it;
     }
     qn += __popc(bm);
     if (!SPEC && qn >= 32) drain(32);
     const uint32_t dm = __ballot_sync(kFull, done);
     if (done) {
-      i = head + __popc(dm & lt);
-      active = i < end;
+      off = head + __popc(dm & lt);
+      active = off < n;
       if (active) setup();
     }
     head += __popc(dm);
   }
   if (!SPEC && qn) drain(qn);
-}
-
-// ---- lockstep schedule (BRNG_LOCKSTEP) ---------------------------------------
-// Iteration k of a warp runs trial 1 of samples beg + 32k + lane in lock step:
-// the parameter loads are coalesced and issued one iteration ahead (the next
-// samples are known), the stores are coalesced, and the only per-iteration
-// bookkeeping is two ballots.  The rare rejected samples (cfg3 1.7%, cfg4 4.2%
-// of samples) are parked with their next trial index in a per-warp retry list
-// and rerun 32 at a time.  Accepted alpha<1 samples are boosted in place when
-// most lanes need it (cfg4: 91% of components) and parked in the boost queue
-// otherwise (cfg3: 36%), so the boost runs as a (nearly) full warp either way.
-// Values are pure functions of (counters, parameters), as for mt_queue.
-// Measured (tools/variant_time.py, identical output hashes): cfg3 0.853 ms
-// (queue) vs 0.912-0.936 (lockstep), cfg4 4.331 vs 4.343-4.346: the lockstep
-// loop carries ~28 constant-bank reloads (LDC/LDCU) per iteration that the
-// queue loop hoists, eating the bookkeeping it saves.  Kept as a build option;
-// the queue is the default.
-#ifndef BRNG_LOCKSTEP
-#define BRNG_LOCKSTEP 0
-#endif
-#ifndef BRNG_INPLACE_MIN
-#define BRNG_INPLACE_MIN 22
-#endif
-[[maybe_unused]] constexpr int kRetryCap = 64;
-
-template <typename P, typename Load, typename Sink>
-__device__ __forceinline__ void mt_lockstep(uint64_t beg, uint64_t end, uint64_t base,
-                                            const RoundKeys& rk, const Tables& tb, Load load,
-                                            Sink sink, uint32_t& nbad, BoostItem* q,
-                                            uint64_t* rq) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t lt = lanemask_lt();
-  uint32_t qn = 0, rn = 0;                           // warp-uniform queue lengths
-  // lanes [0, n) take the last n boost-queue entries, boost and sink them
-  auto drain = [&](uint32_t n) {
-    __syncwarp();
-    if (lane < n) {
-      const BoostItem it = q[qn - n + lane];
-      const uint64_t ii = it.i_t & 0x00FFFFFFFFFFFFFFull;
-      P qa, qb;
-      load(ii, qa, qb);
-      const uint4 wb = philox_block_rk(base + (uint64_t)kStride * ii, rk);
-      sink(ii, mt_boost(wb, it.g, (double)qa, tb) * (double)qb, (uint32_t)(it.i_t >> 56));
-    }
-    qn -= n;
-    __syncwarp();
-  };
-  // lanes [0, n) take the last n retry entries (sample | next trial << 56)
-  // and run their trials until acceptance; boosts in place (rare here)
-  auto retry_pass = [&](uint32_t n) {
-    __syncwarp();
-    const bool act = lane < n;
-    uint64_t e = 0;
-    if (act) e = rq[rn - n + lane];
-    __syncwarp();
-    rn -= n;
-    const uint64_t ii = e & 0x00FFFFFFFFFFFFFFull;
-    uint32_t tt = (uint32_t)(e >> 56);
-    P alr = P(1), ber = P(1);
-    if (act) load(ii, alr, ber);
-    const double al = (double)alr, be = (double)ber;
-    double g = 0.0;
-    bool fin = !act, ok = false;
-    while (__any_sync(kFull, !fin)) {
-      if (!fin) {
-        double d;
-        const uint4 w = philox_block_rk(base + (uint64_t)kStride * ii + tt, rk);
-        if (mt_trial(w, al, d, g, tb)) {
-          fin = true; ok = true;
-        } else if (++tt > kMaxTrial) {
-          fin = true;
-        }
-      }
-    }
-    if (act) {
-      if (!ok) {
-        ++nbad;
-        sink(ii, qnan(), 0u);
-      } else {
-        double v = g;
-        if (al < 1.0) v = mt_boost(philox_block_rk(base + (uint64_t)kStride * ii, rk), g, al, tb);
-        sink(ii, v * be, tt);
-      }
-    }
-  };
-  // parameters of the next iteration, kept in their storage type (converting
-  // at the load would wait for it)
-  P a_nx = P(1), b_nx = P(1);
-  if (beg + lane < end) load(beg + lane, a_nx, b_nx);
-  uint64_t pos = base + (uint64_t)kStride * (beg + lane) + 1;   // trial-1 block of sample i
-  for (uint64_t i0 = beg; i0 < end; i0 += 32, pos += 32ull * kStride) {
-    const uint64_t i = i0 + lane;
-    const double alpha = (double)a_nx, beta = (double)b_nx;
-    if (i + 32 < end) load(i + 32, a_nx, b_nx);
-    bool boost = false, retry = false;
-    double g = 0.0;
-    if (i < end) {
-      const uint4 w = philox_block_rk(pos, rk);
-      const bool valid = isfinite(alpha) && isfinite(beta) && alpha > 0.0 && beta > 0.0;
-      double d;
-      const bool acc = mt_trial(w, alpha, d, g, tb);
-      if (!valid) {
-        ++nbad;
-        sink(i, qnan(), 0u);
-      } else if (!acc) {
-        retry = true;
-      } else if (alpha < 1.0) {
-        boost = true;
-      } else {
-        sink(i, g * beta, 1u);
-      }
-    }
-    const uint32_t rm = __ballot_sync(kFull, retry);
-    if (rm) {
-      if (retry) rq[rn + __popc(rm & lt)] = i | (2ull << 56);
-      rn += __popc(rm);
-    }
-    const uint32_t bm = __ballot_sync(kFull, boost);
-    if (__popc(bm) >= BRNG_INPLACE_MIN) {
-      if (boost) sink(i, mt_boost(philox_block_rk(pos - 1, rk), g, alpha, tb) * beta, 1u);
-    } else if (bm) {
-      if (boost) {
-        BoostItem it;
-        it.g = g;
-#if !BRNG_SLIM_QUEUE
-        it.alpha = alpha; it.beta = beta;
-#endif
-        it.i_t = i | (1ull << 56);
-        q[qn + __popc(bm & lt)] = it;
-      }
-      qn += __popc(bm);
-      if (qn >= 32) drain(32);
-    }
-    if (rn >= 32) retry_pass(32);
-  }
-  while (rn) retry_pass(rn < 32 ? rn : 32);
-  if (qn) drain(qn);
 }
 
 template <typename T>
@@ -345,10 +215,6 @@ template <typename T>
 #endif
 __global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(const __grid_constant__ GammaArgs<T> a) {
   __shared__ BoostItem qs[kThreads / 32][kBoostCap];
-#if BRNG_LOCKSTEP
-  __shared__ uint64_t rqs[kThreads / 32][kRetryCap];
-  uint64_t* rq = rqs[threadIdx.x >> 5];
-#endif
   const Tables tb{};
   BoostItem* q = qs[threadIdx.x >> 5];
   const uint64_t warp = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -365,31 +231,22 @@ __global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(const 
 #else
   for (uint64_t beg = warp * kChunk; beg < a.n; beg += n_warps * kChunk) {
 #endif
-    const uint64_t end = beg + kChunk < a.n ? beg + kChunk : a.n;
-#if BRNG_LOCKSTEP
-    mt_lockstep<T>(
-        beg, end, a.base, a.rk, tb,
-        [&](uint64_t i, T& al, T& be) {
-          al = __ldg(a.alpha + i);
-          be = __ldg(a.beta + i);
-        },
-#else
+    const uint32_t n = (uint32_t)(beg + kChunk < a.n ? kChunk : a.n - beg);
+    const T* al_c = a.alpha + beg;
+    const T* be_c = a.beta + beg;
+    T* out_c = a.out + beg;
+    uint8_t* tr_c = a.trials ? a.trials + beg : nullptr;
     mt_queue<T, BRNG_GAMMA_SPEC != 0>(
-        beg, end, a.base, a.rk, tb,
-        [&](uint64_t i, T& al, T& be) {
-          al = __ldg(a.alpha + i);
-          be = __ldg(a.beta + i);
+        beg, n, a.base, a.rk, tb,
+        [&](uint32_t o, T& al, T& be) {
+          al = __ldg(al_c + o);
+          be = __ldg(be_c + o);
         },
-#endif
-        [&](uint64_t i, double v, uint32_t t) {
-          a.out[i] = (T)v;
-          if (a.trials) a.trials[i] = (uint8_t)t;
+        [&](uint32_t o, double v, uint32_t t) {
+          out_c[o] = (T)v;
+          if (tr_c) tr_c[o] = (uint8_t)t;
         },
-#if BRNG_LOCKSTEP
-        nbad, q, rq);
-#else
         nbad, q);
-#endif
   }
   flush_errors(a.err, nbad);
 }
@@ -436,10 +293,6 @@ template <typename T>
 __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __grid_constant__ DirArgs<T> a) {
   extern __shared__ double gsm[];
   __shared__ BoostItem qs[kDirThreads / 32][kBoostCap];
-#if BRNG_LOCKSTEP
-  __shared__ uint64_t rqs[kDirThreads / 32][kRetryCap];
-  uint64_t* rq = rqs[threadIdx.x >> 5];
-#endif
   const Tables tb{};
   BoostItem* q = qs[threadIdx.x >> 5];
   const uint32_t lane = threadIdx.x & 31;
@@ -464,30 +317,19 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __gri
     const uint64_t row0 = grp * a.rpw;
     const uint64_t rows = a.n_rows - row0 < a.rpw ? a.n_rows - row0 : a.rpw;
     const uint64_t beg = row0 * a.k;
-#if BRNG_LOCKSTEP
-    mt_lockstep<T>(
-        beg, beg + rows * a.k, a.base, a.rk, tb,
-        [&](uint64_t i, T& al, T& be) {
-          al = __ldg(a.alpha + i);
-          be = T(1);
-        },
-#else
+    const T* al_c = a.alpha + beg;
+    uint8_t* tr_c = a.trials ? a.trials + beg : nullptr;
     mt_queue<T, BRNG_DIR_SPEC != 0>(
-        beg, beg + rows * a.k, a.base, a.rk, tb,
-        [&](uint64_t i, T& al, T& be) {
-          al = __ldg(a.alpha + i);
+        beg, (uint32_t)(rows * a.k), a.base, a.rk, tb,
+        [&](uint32_t o, T& al, T& be) {
+          al = __ldg(al_c + o);
           be = T(1);
         },
-#endif
-        [&](uint64_t i, double v, uint32_t t) {
-          g_grp[i - beg] = v;
-          if (a.trials) a.trials[i] = (uint8_t)t;
+        [&](uint32_t o, double v, uint32_t t) {
+          g_grp[o] = v;
+          if (tr_c) tr_c[o] = (uint8_t)t;
         },
-#if BRNG_LOCKSTEP
-        nbad, q, rq);
-#else
         nbad, q);
-#endif
     __syncwarp();
     for (uint64_t r = 0; r < rows; ++r) {
       const double* g_row = g_grp + r * a.k;
@@ -530,18 +372,21 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(const __gr
   for (uint64_t row = a.scratch ? fetch() : warp; row < a.n_rows;
        row = a.scratch ? fetch() : row + n_warps) {
     const uint64_t beg = row * a.k;
-    auto load = [&](uint64_t i, T& al, T& be) {
-      al = __ldg(a.alpha + i);
+    const uint32_t kk = (uint32_t)a.k;                  // k < 2^24 (host-checked)
+    const T* al_c = a.alpha + beg;
+    uint8_t* tr_c = a.trials ? a.trials + beg : nullptr;
+    auto load = [&](uint32_t o, T& al, T& be) {
+      al = __ldg(al_c + o);
       be = T(1);
     };
     double s = 0.0;
     if (sizeof(T) == 4 && a.scratch) {
       // binary32 with scratch: the warp's own row of binary64 Gammas
       double* g_row = a.scratch + warp * a.k;
-      mt_queue<T>(beg, beg + a.k, a.base, a.rk, tb, load,
-               [&](uint64_t i, double v, uint32_t t) {
-                 g_row[i - beg] = v;
-                 if (a.trials) a.trials[i] = (uint8_t)t;
+      mt_queue<T>(beg, kk, a.base, a.rk, tb, load,
+               [&](uint32_t o, double v, uint32_t t) {
+                 g_row[o] = v;
+                 if (tr_c) tr_c[o] = (uint8_t)t;
                },
                nbad, q);
       __syncwarp();                           // the row's Gammas are visible to the warp
@@ -553,10 +398,10 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(const __gr
       for (uint64_t j = lane; j < a.k; j += 32) a.out[beg + j] = (T)(g_row[j] * inv);
       __syncwarp();
     } else if constexpr (sizeof(T) == 8) {
-      mt_queue<T>(beg, beg + a.k, a.base, a.rk, tb, load,
-               [&](uint64_t i, double v, uint32_t t) {
-                 a.out[i] = (T)v;
-                 if (a.trials) a.trials[i] = (uint8_t)t;
+      mt_queue<T>(beg, kk, a.base, a.rk, tb, load,
+               [&](uint32_t o, double v, uint32_t t) {
+                 a.out[beg + o] = (T)v;
+                 if (tr_c) tr_c[o] = (uint8_t)t;
                },
                nbad, q);
       __syncwarp();                           // the row's stores are visible to the warp
@@ -566,14 +411,14 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_2pass_kernel(const __gr
       const double inv = 1.0 / s;
       for (uint64_t j = lane; j < a.k; j += 32) a.out[beg + j] = (T)((double)a.out[beg + j] * inv);
     } else {
-      mt_queue<T>(beg, beg + a.k, a.base, a.rk, tb, load,
-               [&](uint64_t, double v, uint32_t) { s += v; }, nbad, q);
+      mt_queue<T>(beg, kk, a.base, a.rk, tb, load,
+               [&](uint32_t, double v, uint32_t) { s += v; }, nbad, q);
       s = warp_sum(s);
       const double inv = 1.0 / s;
-      mt_queue<T>(beg, beg + a.k, a.base, a.rk, tb, load,
-               [&](uint64_t i, double v, uint32_t t) {
-                 a.out[i] = (T)(v * inv);
-                 if (a.trials) a.trials[i] = (uint8_t)t;
+      mt_queue<T>(beg, kk, a.base, a.rk, tb, load,
+               [&](uint32_t o, double v, uint32_t t) {
+                 a.out[beg + o] = (T)(v * inv);
+                 if (tr_c) tr_c[o] = (uint8_t)t;
                },
                nbad2, q);
     }
