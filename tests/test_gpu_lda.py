@@ -120,3 +120,49 @@ def test_lda_argument_errors():
         assert raw(*a2, 0) == -4                                     # host pointer
         assert B.brng_get_offset(h) == 0
         assert raw(*args[:-1], 0, 0) == 0 and B.brng_get_offset(h) == 0   # n_iter == 0
+
+
+def test_lda_edge_cases():
+    """Empty documents, K = 1, the maximum K, an invalid alpha component."""
+    # empty documents between non-empty ones; K = 3
+    doc_off = torch.tensor([0, 0, 4, 4, 4, 9, 9], dtype=torch.int64)
+    words = torch.tensor([0, 1, 2, 1, 0, 2, 2, 1, 0], dtype=torch.int32)
+    phi = torch.tensor([[0.5, 0.3, 0.2], [0.1, 0.1, 0.8], [0.3, 0.3, 0.4]], dtype=torch.float64)
+    alpha = torch.tensor([0.2, 1.0, 3.0], dtype=torch.float64)
+    z0 = torch.tensor([0, 1, 2, 0, 1, 2, 0, 1, 2], dtype=torch.int16)
+    c = dict(doc_off=doc_off, words=words, phi=phi, z0=z0, n_tokens=9)
+    zg, th, end, errs = _run(c, alpha, z0, 1, B.LDA_INLINE, cursor=77)
+    r = oracle.lda_iteration(77, 3, 77, doc_off.numpy(), words.numpy(), phi.numpy(),
+                             alpha.numpy(), z0.numpy().astype(np.int64))
+    assert np.array_equal(zg, r["z"]) and errs == 0
+    np.testing.assert_allclose(th, r["theta"], rtol=1e-11, atol=0)   # empty docs: Dirichlet(alpha)
+    assert end == 77 + oracle.lda_span(6, 3, 9)
+    # K = 1: theta = g fl(1/g) (within an ulp of 1; R-13), z = 0
+    c1 = dict(doc_off=doc_off, words=words, phi=torch.ones(3, 1, dtype=torch.float64),
+              z0=torch.zeros(9, dtype=torch.int16), n_tokens=9)
+    zg, th, _, _ = _run(c1, torch.ones(1, dtype=torch.float64), c1["z0"], 2, B.LDA_RING)
+    assert np.all(zg == 0) and np.all(np.abs(th - 1.0) <= 2.0**-52)
+    # a component with alpha_k + n_dk not positive-finite (here alpha_1 = NaN):
+    # every document's theta NaN, one error per document, its tokens z = 0
+    bad = alpha.clone(); bad[1] = float("nan")
+    for mode in (B.LDA_INLINE, B.LDA_RING, B.LDA_BULK):
+        zg, th, _, errs = _run(c, bad, z0, 1, mode)
+        assert np.all(np.isnan(th)) and errs == 6 and np.all(zg == 0), mode
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_lda_max_k(mode):
+    """K = 1024 (BRNG_LDA_MAX_K: 12 KB of shared memory per warp): the three
+    sources agree with each other and the oracle on one iteration."""
+    c, _ = _corpus(D=24, K=1024, V=40, L=60, seed=21)
+    alpha = torch.full((1024,), 0.05, dtype=torch.float64)
+    zg, th, _, errs = _run(c, alpha, c["z0"], 1, mode, cursor=5)
+    r = oracle.lda_iteration(77, 3, 5, c["doc_off"].numpy(), c["words"].numpy(), c["phi"].numpy(),
+                             alpha.numpy(), c["z0"].numpy().astype(np.int64))
+    assert errs == 0
+    mism = np.flatnonzero(zg != r["z"])
+    for j in mism:                                      # only rounding ties may differ
+        cum, x = np.array(r["cum"][j]), r["x"][j]
+        assert abs(x - cum[min(int(zg[j]), int(r["z"][j]))]) <= 1e-9 * cum[-1]
+    assert len(mism) <= 1
+    np.testing.assert_allclose(th, r["theta"], rtol=1e-9, atol=0)
