@@ -42,6 +42,39 @@ __global__ void k_gamma(uint64_t seed, uint64_t stream, uint64_t base, const dou
   out[i] = brng_dev::gamma_f64(brng_dev::make_key(seed), stream, base, i, alpha[i], beta[i], &t);
   trials[i] = (unsigned char)t;
 }
+// The split trial (N4, R-33): a "producer" computes the parameter-free parts
+// (trial-1 normal + word, boost log-uniform) into buffers, a "consumer"
+// applies the parameters with mt_accept_z / mt_boost_from_log and runs any
+// later trial with mt_trial -- must equal gamma_f64 bit for bit.
+__global__ void k_gamma_split(uint64_t seed, uint64_t stream, uint64_t base, const double* alpha,
+                              const double* beta, double* out, unsigned char* trials,
+                              uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const brng_dev::Key k = brng_dev::make_key(seed);
+  const uint64_t b0 = base + (uint64_t)brng_dev::kGammaStride * i;
+  // producer part
+  const uint4 w1 = brng_dev::block(k, stream, b0 + 1);
+  const double z1 = brng_dev::mt_normal(w1);
+  const uint32_t w3 = w1.w;
+  const double L = brng_dev::mt_boost_log(brng_dev::block(k, stream, b0));
+  // consumer part
+  const double al = alpha[i], be = beta[i];
+  double d, g = 0.0;
+  unsigned t = 0;
+  if (isfinite(al) && isfinite(be) && al > 0.0 && be > 0.0) {
+    if (brng_dev::mt_accept_z(z1, w3, al, d, g)) {
+      t = 1;
+    } else {
+      for (unsigned tt = 2; tt <= brng_dev::kGammaMaxTrial; ++tt)
+        if (brng_dev::mt_trial(brng_dev::block(k, stream, b0 + tt), al, d, g)) { t = tt; break; }
+    }
+  }
+  if (t == 0) { out[i] = brng_dev::nan_(); trials[i] = 0; return; }
+  if (al < 1.0) g = brng_dev::mt_boost_from_log(L, g, al);
+  out[i] = g * be;
+  trials[i] = (unsigned char)t;
+}
 // Fig. 1 of the paper as a user kernel: one chain per thread.
 __global__ void k_gibbs(uint64_t seed, uint64_t stream_id, uint64_t base, uint64_t n_chains,
                         uint64_t n_sweeps, double* out_x, double* out_y) {
@@ -119,6 +152,11 @@ int dev_fill32(int dist, uint64_t seed, uint64_t stream, uint64_t base, const fl
 int dev_gamma(uint64_t seed, uint64_t stream, uint64_t base, const double* a, const double* b,
               double* out, unsigned char* tr, uint64_t n, void* s) {
   k_gamma<<<grid(n), 256, 0, (cudaStream_t)s>>>(seed, stream, base, a, b, out, tr, n);
+  return (int)cudaGetLastError();
+}
+int dev_gamma_split(uint64_t seed, uint64_t stream, uint64_t base, const double* a,
+                    const double* b, double* out, unsigned char* tr, uint64_t n, void* s) {
+  k_gamma_split<<<grid(n), 256, 0, (cudaStream_t)s>>>(seed, stream, base, a, b, out, tr, n);
   return (int)cudaGetLastError();
 }
 int dev_math(int fn, const double* x, const uint32_t* w, double* out, uint64_t n, void* s) {

@@ -104,6 +104,29 @@ def test_gamma_getter_bit_exact(user_lib):
     assert torch.equal(t1, t2) and torch.equal(o1, o2)
 
 
+def test_split_trial_producer_consumer_bit_exact(user_lib):
+    """mt_normal / mt_accept_z / mt_boost_log / mt_boost_from_log (the
+    producer/consumer split of a trial, N4 R-33) composed in a user kernel
+    equal the bulk Gamma call bit for bit, decisions included; invalid
+    parameters give NaN with trial 0 (the bulk call also counts them)."""
+    n = 40_003
+    p = workloads.cfg3_params(n, seed=13, device=dev())
+    p["alpha"][7] = -1.0
+    p["beta"][9] = float("nan")
+    o1 = torch.empty(n, dtype=torch.float64, device=dev())
+    t1 = torch.empty(n, dtype=torch.uint8, device=dev())
+    user_lib.dev_gamma_split.argtypes = user_lib.dev_gamma.argtypes
+    assert user_lib.dev_gamma_split(13, 2, 512, p["alpha"].data_ptr(), p["beta"].data_ptr(),
+                                    o1.data_ptr(), t1.data_ptr(), n, _s()) == 0
+    with handle(13, 2, 512) as h:
+        o2 = torch.empty(n, dtype=torch.float64, device=dev())
+        t2 = torch.empty(n, dtype=torch.uint8, device=dev())
+        B.brng_gamma_f64(h, p["alpha"], p["beta"], o2, n, t2)
+    assert torch.equal(t1, t2)
+    assert torch.equal(torch.nan_to_num(o1, nan=-7.0), torch.nan_to_num(o2, nan=-7.0))
+    assert (t1 > 1).any()                               # later trials exercised
+
+
 def test_fig1_user_gibbs_loop_matches_oracle_and_bulk(user_lib):
     nc, ns = 1024, 200
     ox = torch.empty(ns, nc, dtype=torch.float64, device=dev())
