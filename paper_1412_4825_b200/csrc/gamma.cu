@@ -32,9 +32,6 @@ constexpr int kThreads = 256;
 #define BRNG_GAMMA_CHUNK 2048
 #endif
 constexpr uint64_t kChunk = BRNG_GAMMA_CHUNK;
-#ifndef BRNG_F32T_PROBE
-#define BRNG_F32T_PROBE 0     // N3 cost probe only (see mt_queue)
-#endif
 #ifndef BRNG_GAMMA_SPEC
 #define BRNG_GAMMA_SPEC 0     // speculative boosts for Gamma (cfg3: 36% boosted)
 #endif
@@ -153,34 +150,7 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint32_t n, uint64_t base
       alpha = (double)alpha_r;
       const double beta = (double)beta_r;
       const bool valid = isfinite(alpha) && isfinite(beta) && alpha > 0.0 && beta > 0.0;
-#if BRNG_F32T_PROBE
-      // N3 cost probe (NOT a correct path: no binary64 fallback): the trial
-      // in binary32 -- logf, sqrtf, the binary32 table sincos, t, v, g and
-      // the screen in binary32 -- to bound what a binary32 trial can save
-      bool acc;
-      {
-        const float omu = (float)brng_dev::dm::one_minus_u53(w.x, w.y);
-        const float r = sqrtf(-2.0f * logf(omu));
-        float sn, cs;
-        brng_dev::dm::sincos2pi_u24(w.z, &sn, &cs);
-        const float z = r * cs;
-        const float af = (float)alpha_r;
-        const float ap = af < 1.0f ? af + 1.0f : af;
-        const float df = ap - (1.0f / 3.0f);
-        const float cf = rsqrtf(9.0f * df);
-        const float tf = fmaf(cf, z, 1.0f);
-        const float v = tf * tf * tf;
-        const float z2h = 0.5f * z * z;
-        const float lnt = brng_dev::dm::ln_approx_f32(tf);
-        const float lnu = brng_dev::dm::ln_approx_f32(fmaf(__uint2float_rn(~w.w), 0x1p-32f, 0x1p-32f));
-        const float m = fmaf(df, fmaf(3.0f, lnt, 1.0f - v), z2h) - lnu;
-        acc = tf > 0.0f && m > 0.0f;
-        g = (double)(df * v);
-        d = (double)df;
-      }
-#else
       const bool acc = mt_trial(w, alpha, d, g, tb);
-#endif
       if (!valid) {
         done = true; t = 0; ++nbad;
       } else if (acc) {
