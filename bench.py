@@ -28,7 +28,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -552,6 +551,7 @@ def gpu_arm(args):
     e2e = None
     if not args.no_e2e:
         e2e = e2e_run(wl, torch, B, args, allreduce, world, dist)
+    wl_launches = wl.launches_per_step
     wl.destroy()
     del wl
     torch.cuda.empty_cache()
@@ -590,7 +590,7 @@ def gpu_arm(args):
                     "note": "this rank's per-step device times; value uses the mean over "
                             "all steps, max over ranks"},
         "determinism": determinism,
-        "gpu_launches": 8 * args.steps,
+        "gpu_launches": wl_launches * args.steps,
         "device_errors": errs,
         "clocks": clk,
     }
@@ -599,7 +599,7 @@ def gpu_arm(args):
     if e2e is not None:
         out["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args.cpu_budget_s)
+        out["cpu_baseline"] = cpu_baseline()
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -745,9 +745,6 @@ def cpu_model():
     return "unknown"
 
 
-FULL_UNITS = None
-
-
 def full_units():
     """Units of each config in one full step (chains, samples, documents)."""
     import workloads as W
@@ -856,7 +853,7 @@ def _mix_value(res, units_full):
     return sum(units_full[k] * spu[k] for k in units_full) / t / 1e9
 
 
-def cpu_baseline(budget_s=None):
+def cpu_baseline():
     """The oracle as it stands on the GPU box's host cores:
     cfg1-cfg4 at FULL size on all P cores; cfg5 on a stride subset of its
     chains (every 16th block of 64 chains = 1/16, full 4096 sweeps); each
@@ -974,8 +971,6 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None,
                     help="e2e steps (default: --steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=15.0, help="(unused; kept for CLI "
-                    "compatibility)")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
                     help="--impl reference: total oracle seconds for W + K steps")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
