@@ -284,7 +284,10 @@ BRNG_API int brng_gibbs_triangle(brng_t h, uint64_t n_chains, uint64_t n_sweeps,
  * library's Dirichlet and uniform-fill kernels into scratch, then the
  * consumer).  All three give the same bits.  A component whose alpha_k + n_dk
  * is not positive and finite makes the document's theta NaN (counted once
- * per such component) and its tokens' z = 0.  k <= BRNG_LDA_MAX_K.  RING/BULK use handle-owned scratch
+ * per such component) and its tokens' z = 0.  A document range that
+ * decreases or passes n_tokens is counted and treated as empty; a token with
+ * words[j] >= v is counted and keeps its z (no out-of-range access either
+ * way); topics z >= k count as topic k-1.  k <= BRNG_LDA_MAX_K.  RING/BULK use handle-owned scratch
  * (two slots of 20 n_docs k + 8 n_tokens bytes / 16 n_docs k + 8 n_tokens),
  * grown on the first call of a size (not inside a graph capture:
  * BRNG_ERR_STATE).  Asynchronous on the handle's stream. */

@@ -103,7 +103,13 @@ __global__ void __launch_bounds__(kLdaThreads) lda_consumer_kernel(const __grid_
     if (lane == 0) dd = atomicAdd(a.work, 1ull);
     const uint64_t d = __shfl_sync(kFull, dd, 0);
     if (d >= a.n_docs) break;
-    const uint64_t j0 = a.doc_off[d], j1 = a.doc_off[d + 1];
+    uint64_t j0 = a.doc_off[d], j1 = a.doc_off[d + 1];
+    // a malformed document range (decreasing, or past n_tokens) is counted
+    // and treated as empty: no access outside the caller's arrays
+    if (j1 < j0 || j1 > a.n_tokens) {
+      nbad += lane == 0 ? 1u : 0u;
+      j0 = j1 = 0;
+    }
     if (SRC != 2) {
       for (uint32_t k = lane; k < K; k += 32) cnt[k] = 0;
       __syncwarp();
@@ -141,7 +147,12 @@ __global__ void __launch_bounds__(kLdaThreads) lda_consumer_kernel(const __grid_
     __syncwarp();
     for (uint64_t j = j0 + lane; j < j1; j += 32) {
       const double u = SRC == 0 ? brng_dev::std_uniform_f64(key, a.stream, ubase, j) : a.ubuf[j];
-      const double* ph = a.phi + (uint64_t)a.words[j] * K;
+      const uint32_t w = a.words[j];
+      if (w >= a.v) {                         // word id out of range: counted, z unchanged
+        ++nbad;
+        continue;
+      }
+      const double* ph = a.phi + (uint64_t)w * K;
       a.z[j] = (uint16_t)categorical(th, ph, K, u);
     }
     __syncwarp();
@@ -193,7 +204,9 @@ __global__ void __launch_bounds__(kLdaThreads) lda_rows_kernel(const __grid_cons
   for (uint64_t d = warp; d < a.n_docs; d += nw) {
     for (uint32_t k = lane; k < K; k += 32) cnt[k] = 0;
     __syncwarp();
-    for (uint64_t j = a.doc_off[d] + lane; j < a.doc_off[d + 1]; j += 32) {
+    uint64_t j0 = a.doc_off[d], j1 = a.doc_off[d + 1];
+    if (j1 < j0 || j1 > a.n_tokens) j0 = j1 = 0;     // malformed range (counted by the consumer)
+    for (uint64_t j = j0 + lane; j < j1; j += 32) {
       const uint32_t zz = a.z[j];
       atomicAdd(&cnt[zz < K ? zz : K - 1], 1u);
     }

@@ -166,3 +166,25 @@ def test_lda_max_k(mode):
         assert abs(x - cum[min(int(zg[j]), int(r["z"][j]))]) <= 1e-9 * cum[-1]
     assert len(mism) <= 1
     np.testing.assert_allclose(th, r["theta"], rtol=1e-9, atol=0)
+
+
+def test_lda_malformed_inputs_are_counted_not_followed():
+    """A decreasing / out-of-range document range and out-of-range word ids
+    are counted in the device error counter and skipped (no out-of-bounds
+    access); the other documents are unaffected."""
+    c, alpha = _corpus(D=6, K=4, V=8, L=5, seed=3)
+    good = _run(c, alpha, c["z0"], 1, B.LDA_INLINE, cursor=9)
+    bad = dict(c)
+    off = c["doc_off"].clone()
+    off[3] = off[4] + 1000                     # doc 2 ends past doc 3's end (decreasing next)
+    bad["doc_off"] = off
+    zg, _, _, errs = _run(bad, alpha, c["z0"], 1, B.LDA_INLINE, cursor=9)
+    assert errs >= 2                           # docs 2 and 3 malformed
+    keep = np.r_[int(off[0]):int(off[2]), int(c["doc_off"][4]):c["n_tokens"]]
+    assert np.array_equal(zg[keep], good[0][keep])
+    w = c["words"].clone()
+    w[0] = 8                                   # == v: out of range
+    bad2 = dict(c, words=w)
+    zg2, _, _, errs2 = _run(bad2, alpha, c["z0"], 1, B.LDA_BULK, cursor=9)
+    assert errs2 == 1 and zg2[0] == int(c["z0"][0])
+    assert np.array_equal(zg2[1:], good[0][1:])
