@@ -738,7 +738,8 @@ int brng_lda_gibbs(brng_t h, uint64_t n_docs, uint32_t k, uint32_t v, uint64_t n
   for (const void* p : {(const void*)doc_off, (const void*)words, (const void*)phi,
                         (const void*)alpha, (const void*)z, (const void*)theta})
     if (p && !is_device_ptr(p)) return BRNG_ERR_PARAM;          // device pointers only
-  if (!mul_ok(n_docs, k) || !mul_ok(n_docs * k, BRNG_GAMMA_STRIDE)) return BRNG_ERR_SIZE;
+  if (!mul_ok(n_docs, k) || !mul_ok(n_docs * k, BRNG_GAMMA_STRIDE) || !mul_ok(n_tokens, 16))
+    return BRNG_ERR_SIZE;
   const uint64_t dk = n_docs * k;
   const uint64_t gspan = dk * BRNG_GAMMA_STRIDE;
   const uint64_t uspan = n_tokens / 2 + (n_tokens % 2);
@@ -790,14 +791,22 @@ int brng_lda_gibbs(brng_t h, uint64_t n_docs, uint32_t k, uint32_t v, uint64_t n
     }
   } else {
     if (!h->lda_ready) {
-      if (cudaStreamCreateWithFlags(&h->s_prod, cudaStreamNonBlocking) != cudaSuccess)
+      // all-or-nothing: a partial failure releases what was created
+      cudaStream_t sp = nullptr;
+      cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+      bool ok = cudaStreamCreateWithFlags(&sp, cudaStreamNonBlocking) == cudaSuccess;
+      for (int b = 0; b < 5 && ok; ++b)
+        ok = cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming) == cudaSuccess;
+      if (!ok) {
+        for (cudaEvent_t x : ev)
+          if (x) cudaEventDestroy(x);
+        if (sp) cudaStreamDestroy(sp);
         return BRNG_ERR_CUDA;
-      for (int b = 0; b < 2; ++b)
-        if (cudaEventCreateWithFlags(&h->ev_prod[b], cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&h->ev_cons[b], cudaEventDisableTiming) != cudaSuccess)
-          return BRNG_ERR_CUDA;
-      if (cudaEventCreateWithFlags(&h->ev_lda, cudaEventDisableTiming) != cudaSuccess)
-        return BRNG_ERR_CUDA;
+      }
+      h->s_prod = sp;
+      h->ev_prod[0] = ev[0]; h->ev_prod[1] = ev[1];
+      h->ev_cons[0] = ev[2]; h->ev_cons[1] = ev[3];
+      h->ev_lda = ev[4];
       h->lda_ready = true;
     }
     struct Slot { double* zb; uint32_t* w3; double* lb; double* ub; } sl[2];
