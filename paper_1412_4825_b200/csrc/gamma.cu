@@ -344,173 +344,6 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __gri
   flush_errors(a.err, nbad);
 }
 
-// ---- warp-specialised Dirichlet rows (BRNG_DIR_WS) --------------------------
-// Each CTA holds kWsPairs pairs of a PRODUCER warp and a CONSUMER warp.  A
-// pair takes row groups from the work counter.  The producer computes every
-// component's parameter-free deviates in index order, 32 components (one per
-// lane) per chunk: the trial-1 normal z and word w3 (mt_normal) and the boost
-// log-uniform ln(1-u) (mt_boost_log), into a double-buffered shared-memory
-// chunk.  The consumer runs the components in lock step, one chunk per step:
-// it applies alpha (mt_accept_z, mt_boost_from_log -- every lane, no
-// divergent region), stages accepted Gammas in the row buffer, and parks the
-// rare rejected components (with their ln(1-u)) in a retry list rerun 32 at a
-// time with inline trials >= 2.  Then the rows are normalised as in
-// dirichlet_smem_kernel.  Chunks are handed over with named barriers (FULL:
-// producer arrive / consumer sync; EMPTY: consumer arrive / producer sync).
-// Values: the same functions in the same order as the other kernels
-// (mt_trial = mt_accept_z(mt_normal(w), w.w, ...)), so bit-identical.
-#ifndef BRNG_DIR_WS
-#define BRNG_DIR_WS 0
-#endif
-constexpr int kWsPairs = 2;
-constexpr int kWsThreads = kWsPairs * 64;
-struct WsEntry {
-  double z, L;
-  uint32_t w3, pad;
-};
-struct WsRetry {
-  double L;
-  uint32_t off, t;
-};
-constexpr int kWsRetryCap = 64;
-
-__device__ __forceinline__ void ws_bar_sync(uint32_t id) {
-  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
-}
-__device__ __forceinline__ void ws_bar_arrive(uint32_t id) {
-  asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory");
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kWsThreads) dirichlet_ws_kernel(const __grid_constant__ DirArgs<T> a) {
-  extern __shared__ double gsm[];                     // [pair][rpw * k] staged Gammas
-  __shared__ WsEntry ent[kWsPairs][2][32];
-  __shared__ WsRetry rq[kWsPairs][kWsRetryCap];
-  __shared__ unsigned long long grp_sh[kWsPairs];
-  const Tables tb{};
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t pair = warp >> 1;
-  const bool producer = (warp & 1) == 0;
-  const uint32_t lt = lanemask_lt();
-  // named barrier ids (0 is __syncthreads): per pair GRP, FULL0/1, EMPTY0/1
-  const uint32_t id_grp = 1 + pair * 5, id_full = id_grp + 1, id_empty = id_grp + 3;
-  double* g_grp = gsm + (uint64_t)pair * a.rpw * a.k;
-  const uint64_t n_groups = (a.n_rows + a.rpw - 1) / a.rpw;
-  uint32_t nbad = 0;
-  uint32_t seq = 0;                                   // chunks handed over by this pair
-  for (;;) {
-    if (!producer && lane == 0) grp_sh[pair] = atomicAdd(a.work, 1ull);
-    ws_bar_sync(id_grp);
-    const uint64_t grp = grp_sh[pair];
-    if (grp >= n_groups) break;
-    const uint64_t row0 = grp * a.rpw;
-    const uint64_t rows = a.n_rows - row0 < a.rpw ? a.n_rows - row0 : a.rpw;
-    const uint64_t beg = row0 * a.k;
-    const uint32_t n = (uint32_t)(rows * a.k);
-    const uint32_t n_chunks = (n + 31) / 32;
-    const uint64_t base_c = a.base + (uint64_t)kStride * beg;
-    if (producer) {
-      for (uint32_t c = 0; c < n_chunks; ++c, ++seq) {
-        const uint32_t b = seq & 1;
-        if (seq >= 2) ws_bar_sync(id_empty + b);      // the consumer is done with chunk seq - 2
-        const uint32_t off = c * 32 + lane;
-        if (off < n) {
-          const uint64_t pos = base_c + ((uint64_t)off << 8);
-          const uint4 w1 = philox_block_rk(pos + 1, a.rk);
-          WsEntry e;
-          e.z = brng_dev::mt_normal(w1, tb);
-          e.w3 = w1.w;
-          e.L = brng_dev::mt_boost_log(philox_block_rk(pos, a.rk), tb);
-          e.pad = 0;
-          ent[pair][b][lane] = e;
-        }
-        ws_bar_arrive(id_full + b);
-      }
-      continue;
-    }
-    // ---- consumer ----
-    const T* al_c = a.alpha + beg;
-    uint8_t* tr_c = a.trials ? a.trials + beg : nullptr;
-    uint32_t rn = 0;                                  // retry list length (warp-uniform)
-    auto retry_pass = [&](uint32_t k) {               // lanes [0, k) take the last k entries
-      __syncwarp();
-      const bool act = lane < k;
-      WsRetry r{0.0, 0u, 0u};
-      if (act) r = rq[pair][rn - k + lane];
-      __syncwarp();
-      rn -= k;
-      if (act) {
-        const double al = (double)__ldg(al_c + r.off);
-        const uint64_t b0 = base_c + ((uint64_t)r.off << 8);
-        double d, g = 0.0;
-        uint32_t t = 0;
-        for (uint32_t tt = r.t; tt <= kMaxTrial; ++tt)
-          if (mt_trial(philox_block_rk(b0 + tt, a.rk), al, d, g, tb)) { t = tt; break; }
-        if (t == 0) {
-          ++nbad;
-          g_grp[r.off] = qnan();
-        } else {
-          g_grp[r.off] = al < 1.0 ? brng_dev::mt_boost_from_log(r.L, g, al, tb) : g;
-        }
-        if (tr_c) tr_c[r.off] = (uint8_t)t;
-      }
-    };
-    T a_nx = T(1);
-    if (lane < n) a_nx = __ldg(al_c + lane);
-    for (uint32_t c = 0; c < n_chunks; ++c, ++seq) {
-      const uint32_t b = seq & 1;
-      const uint32_t off = c * 32 + lane;
-      const bool act = off < n;
-      const double alpha = (double)a_nx;
-      if (off + 32 < n) a_nx = __ldg(al_c + off + 32);   // next chunk's parameter
-      ws_bar_sync(id_full + b);
-      const WsEntry e = ent[pair][b][lane];
-      ws_bar_arrive(id_empty + b);
-      bool retry = false;
-      if (act) {
-        const bool valid = isfinite(alpha) && alpha > 0.0;
-        double d, g = 0.0;
-        const bool acc = brng_dev::mt_accept_z(e.z, e.w3, alpha, d, g);
-        const double gb = brng_dev::mt_boost_from_log(e.L, g, alpha, tb);
-        if (!valid) {
-          ++nbad;
-          g_grp[off] = qnan();
-          if (tr_c) tr_c[off] = 0;
-        } else if (acc) {
-          g_grp[off] = alpha < 1.0 ? gb : g;
-          if (tr_c) tr_c[off] = 1;
-        } else {
-          retry = true;
-        }
-      }
-      const uint32_t rm = __ballot_sync(kFull, retry);
-      if (retry) {
-        WsRetry r;
-        r.L = e.L; r.off = off; r.t = 2;
-        rq[pair][rn + __popc(rm & lt)] = r;
-      }
-      rn += __popc(rm);
-      if (rn >= 32) retry_pass(32);
-    }
-    while (rn) retry_pass(rn < 32 ? rn : 32);
-    __syncwarp();
-    for (uint64_t r = 0; r < rows; ++r) {
-      const double* g_row = g_grp + r * a.k;
-      double sum = 0.0;
-      for (uint64_t j = lane; j < a.k; j += 32) sum += g_row[j];
-      sum = warp_sum(sum);
-      const double inv = 1.0 / sum;
-      for (uint64_t j = lane; j < a.k; j += 32) a.out[beg + r * a.k + j] = (T)(g_row[j] * inv);
-    }
-    __syncwarp();
-  }
-  // the producer matches the consumer's last EMPTY arrivals
-  if (producer) {
-    for (uint32_t q = seq >= 2 ? seq - 2 : 0; q < seq; ++q) ws_bar_sync(id_empty + (q & 1));
-  }
-  flush_errors(a.err, nbad);
-}
-
 // Any K: two passes over the row.  binary64 output: the first pass stores the
 // unnormalised Gammas in the output row itself, the second rescales them in
 // place.  binary32 output: a Gamma may not be representable in binary32
@@ -652,29 +485,6 @@ cudaError_t dirichlet_typed(const T* alpha, uint64_t n_rows, uint64_t k, T* out,
       if (e != cudaSuccess) return e;
     }
     const uint64_t groups = (n_rows + a.rpw - 1) / a.rpw;
-#if BRNG_DIR_WS
-    {
-      const size_t smem_ws = (size_t)kWsPairs * a.rpw * k * sizeof(double);
-      if (smem_ws > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(dirichlet_ws_kernel<T>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem_ws);
-        if (e != cudaSuccess) return e;
-      }
-      int per_sm = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dirichlet_ws_kernel<T>,
-                                                        kWsThreads, smem_ws) != cudaSuccess ||
-          per_sm < 1)
-        per_sm = 1;
-      const uint64_t cap = (uint64_t)ctx.num_sms * per_sm;
-      const uint64_t want = (groups + kWsPairs - 1) / kWsPairs;
-      cudaError_t e0 = cudaMemsetAsync(ctx.work, 0, sizeof(unsigned long long), ctx.stream);
-      if (e0 != cudaSuccess) return e0;
-      const unsigned g = (unsigned)(want < cap ? want : cap);
-      dirichlet_ws_kernel<T><<<g, kWsThreads, smem_ws, ctx.stream>>>(a);
-      return cudaGetLastError();
-    }
-#endif
     const uint64_t ctas = (groups + 3) / 4;
 #if BRNG_GAMMA_DYN
     // one resident wave of CTAs; warps take row groups from a counter
