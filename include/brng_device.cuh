@@ -18,6 +18,12 @@
  *
  * The library's own kernels are built from the same primitives (philox10,
  * u24/u53/u32d, mt_trial).
+ *
+ * A Gamma trial also splits into its parameter-free part and the part that
+ * uses alpha (mt_normal + mt_accept_z; mt_boost_log + mt_boost_from_log), so
+ * a producer can precompute the former into a buffer and a consumer apply
+ * the latter with bit-identical results -- the "BatchRNG as asynchronous
+ * service" reading R-33 (brng_lda_gibbs's RING mode does this).
  */
 #ifndef BRNG_DEVICE_CUH
 #define BRNG_DEVICE_CUH
