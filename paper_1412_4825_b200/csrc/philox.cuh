@@ -52,24 +52,6 @@ inline RoundKeys make_round_keys(uint32_t k0, uint32_t k1, uint64_t stream) {
   return rk;
 }
 // Block `pos` of the stream rk was made for.
-#ifdef BRNG_PROBE_FIXED_SEED
-// EXPERIMENT ONLY (tools/variant_time.py): round keys of a compile-time seed
-// and stream 0 as immediates, to measure what the runtime keys' constant-bank
-// reloads cost.  Wrong for any other seed.
-__device__ __forceinline__ uint4 philox_block_rk(uint64_t pos, const RoundKeys&) {
-  constexpr uint64_t kSeed = BRNG_PROBE_FIXED_SEED;
-  constexpr uint32_t k0 = (uint32_t)kSeed, k1 = (uint32_t)(kSeed >> 32);
-  const uint64_t p0 = (uint64_t)kPhiloxM0 * (uint32_t)pos;
-  uint4 c;
-  c.x = k0 ^ (uint32_t)(pos >> 32);          // hi(M1 * 0) = 0
-  c.y = 0u;
-  c.z = (uint32_t)(p0 >> 32) ^ k1;
-  c.w = (uint32_t)p0;
-#pragma unroll
-  for (int r = 1; r < 10; ++r) c = philox_round(c, k0 + (uint32_t)r * kPhiloxW0, k1 + (uint32_t)r * kPhiloxW1);
-  return c;
-}
-#else
 __device__ __forceinline__ uint4 philox_block_rk(uint64_t pos, const RoundKeys& rk) {
   const uint64_t p0 = (uint64_t)kPhiloxM0 * (uint32_t)pos;
   uint4 c;
@@ -81,7 +63,6 @@ __device__ __forceinline__ uint4 philox_block_rk(uint64_t pos, const RoundKeys& 
   for (int r = 1; r < 10; ++r) c = philox_round(c, rk.k0[r], rk.k1[r]);
   return c;
 }
-#endif
 
 // ---- warp helpers -----------------------------------------------------------
 __device__ __forceinline__ uint32_t lanemask_lt() {
