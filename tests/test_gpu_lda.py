@@ -188,3 +188,65 @@ def test_lda_malformed_inputs_are_counted_not_followed():
     zg2, _, _, errs2 = _run(bad2, alpha, c["z0"], 1, B.LDA_BULK, cursor=9)
     assert errs2 == 1 and zg2[0] == int(c["z0"][0])
     assert np.array_equal(zg2[1:], good[0][1:])
+
+
+def _phi_at(phi, byte_off):
+    """phi's values in device memory starting byte_off bytes past a 256-byte
+    boundary (the consumer reads rows with 256-bit loads only when phi is
+    32-byte aligned and K % 4 == 0)."""
+    n = phi.numel()
+    buf = torch.empty(n + 64, dtype=torch.float64, device=dev())
+    v = buf[byte_off // 8: byte_off // 8 + n].view(phi.shape)
+    v.copy_(phi.to(dev()))
+    return v
+
+
+@pytest.mark.parametrize("K", [64, 40, 7])
+def test_categorical_load_paths_agree(K):
+    """The 256-bit-load search (K % 4 == 0, phi 32-byte aligned) and the
+    scalar search (phi 8 bytes off) give the same topics bit for bit, and
+    both match the oracle's plain sequential search up to rounding ties of
+    theta."""
+    c, alpha = _corpus(D=400, K=K, V=120, L=40, seed=31 + K)
+    D, T = len(c["doc_off"]) - 1, c["n_tokens"]
+    res = []
+    for off in (0, 8):
+        zd = c["z0"].to(dev()).clone()
+        th = torch.empty(D, K, dtype=torch.float64, device=dev())
+        with handle(77, 3, 11) as h:
+            B.brng_lda_gibbs(h, D, K, c["phi"].shape[0], T, c["doc_off"].to(dev()),
+                             c["words"].to(dev()), _phi_at(c["phi"], off), alpha.to(dev()), zd, th,
+                             1, B.LDA_INLINE)
+            assert B.brng_device_errors(h) == 0
+        res.append((zd.cpu().numpy().astype(np.int64), th.cpu().numpy()))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    r = oracle.lda_iteration(77, 3, 11, c["doc_off"].numpy(), c["words"].numpy(),
+                             c["phi"].numpy(), alpha.numpy(), c["z0"].numpy().astype(np.int64))
+    mism = np.flatnonzero(res[0][0] != r["z"])
+    for j in mism:
+        cum, x = np.array(r["cum"][j]), r["x"][j]
+        assert abs(x - cum[min(int(res[0][0][j]), int(r["z"][j]))]) <= 1e-9 * cum[-1]
+    assert len(mism) <= 2
+
+
+def test_categorical_negative_weights_take_the_plain_search():
+    """phi entries with a set sign bit (negative values, -0.0) make the running
+    sums non-monotone; the consumer then runs the plain sequential search, so
+    the topics still equal the oracle's first k with x < c_k (given theta)."""
+    c, alpha = _corpus(D=300, K=32, V=50, L=30, seed=5)
+    phi = c["phi"].clone()
+    phi[::3, 5] *= -1.0                       # every third word: a negative weight
+    phi[1::7, 9] = -0.0
+    c2 = dict(c, phi=phi)
+    zg, th, _, errs = _run(c2, alpha, c["z0"], 1, B.LDA_BULK, cursor=21)
+    assert errs == 0
+    r = oracle.lda_iteration(77, 3, 21, c["doc_off"].numpy(), c["words"].numpy(), phi.numpy(),
+                             alpha.numpy(), c["z0"].numpy().astype(np.int64))
+    # recompute the oracle's search from the GPU's own theta: exact equality
+    words, doc_off = c["words"].numpy(), c["doc_off"].numpy()
+    u = oracle.std_uniform(77, 3, 21 + oracle.GAMMA_STRIDE * th.size, c["n_tokens"], np.float64)
+    for d in range(len(doc_off) - 1):
+        for j in range(doc_off[d], doc_off[d + 1]):
+            zj, _, _ = oracle.lda_categorical(th[d], phi.numpy()[words[j]], u[j])
+            assert zg[j] == zj, (d, j)
+    assert (zg != r["z"]).mean() < 0.01
