@@ -317,11 +317,12 @@ cudaError_t launch_lda_consumer(int src, const LdaArgs& a, const Ctx& ctx) {
   cudaError_t e = cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), ctx.stream);
   if (e != cudaSuccess) return e;
   const uint64_t want = (a.n_docs + 3) / 4;
-  // The categorical step reads the token's phi row twice (total, then
-  // search): the second read should hit L1.  Left to itself the driver gives
-  // a low-register consumer (BULK: 31 registers) a shared-memory carve-out
-  // for 16 CTAs/SM, which leaves little L1 (K = 256: 5.4 vs 3.0 ms per
-  // iteration); every consumer gets the carve-out for kLdaCtasPerSm CTAs.
+  // Shared-memory carve-out for kLdaCtasPerSm CTAs/SM.  Left to itself the
+  // driver gives a low-register consumer (BULK: 42 registers) a carve-out
+  // for 16 CTAs/SM, which leaves little L1 for the phi rows.  Carve-outs for
+  // 4 / 8 / 12 / 16 CTAs measured 1.74 / 1.62 / 1.62 / 1.70 ms (inline) and
+  // 1.73 / 1.69 / 1.78 / 2.35 ms (bulk) per iteration at the bench shape
+  // (profiles/r02_lda_carveout.txt).
   constexpr int kLdaCtasPerSm = 8;
   const int carve = (int)std::min<size_t>(
       100, (kLdaCtasPerSm * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
