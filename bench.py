@@ -42,6 +42,7 @@ METRIC = "Gsamples/s varying-param Gamma & Gibbs at 1/2/4/8 B200; % of roofline"
 UNIT = "Gsamples/s"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0          # B200_PROFILING.md fallback
+NOMINAL_HBM_GBS = 8000.0           # BASELINE north_star "roughly 8 TB/s" (report both)
 SMS, SMSP, LANES = 148, 4, 32
 # Gibbs roofline: the sweep is bound by the B200
 # FMA-heavy pipe, which runs every fp64 op (64 lanes/clk/SM) and the 32x32->64
@@ -486,7 +487,8 @@ def gpu_arm(args):
         d = {"ms": round(per[n], 4), "Gsamples_per_s": round(wl.samples[n] / t / 1e9, 3)}
         if n in ("cfg2_gaussian", "cfg2_uniform"):
             gbs = 12.0 * wl.samples[n] / t / 1e9
-            d.update(bound="hbm", GB_per_s=round(gbs, 1), frac=round(gbs / hbm_peak, 4))
+            d.update(bound="hbm", GB_per_s=round(gbs, 1), frac=round(gbs / hbm_peak, 4),
+                     frac_nominal_8TBs=round(gbs / NOMINAL_HBM_GBS, 4))
         elif n in mix:
             mt, fb, per_sample = mix[n]
             slots, frac, issue_peak = gamma_models(mt, fb, per_sample, wl.samples[n], t, sm_hz)
