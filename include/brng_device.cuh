@@ -126,6 +126,8 @@ static __constant__ double kC[kNumConst] = {
 // the same arrays elsewhere (e.g. shared memory) behind the same interface:
 // same values, so the same results bit for bit.
 struct GlobalTables {
+  // constant i of kC (a table type may keep some of them in registers)
+  __device__ __forceinline__ double k(int i) const { return kC[i]; }
   __device__ __forceinline__ double2 ln(int j) const { return __ldg(&tab::kLn[j]); }
   __device__ __forceinline__ double2 cs(uint32_t j) const { return __ldg(&tab::kCos[j]); }
   __device__ __forceinline__ double exp2(int j) const { return __ldg(&tab::kExp2[j]); }
@@ -153,10 +155,10 @@ __device__ __forceinline__ double ln_pos(double x, const Tab& tb = Tab()) {
   const int hx = __double2hiint(x);
   const int e = (hx - 0x3FE6A09E) >> 20;
   const double m = __hiloint2double(hx - e * (1 << 20), __double2loint(x));
-  const int j = __double2loint(fma(m, 128.0, kC[kRndM128]));
+  const int j = __double2loint(fma(m, 128.0, tb.k(kRndM128)));
   const double2 ct = tb.ln(j + tab::kLnOff);
   const double r = fma(m, ct.x, -1.0);
-  double q = fma(r, kC[kL7], kC[kL6]);
+  double q = fma(r, tb.k(kL7), kC[kL6]);
   q = fma(r, q, kC[kL5]);
   q = fma(r, q, kC[kL4]);
   q = fma(r, q, kC[kL3]);
@@ -174,8 +176,8 @@ __device__ __forceinline__ double cos2pi_u32(uint32_t w, const Tab& tb = Tab()) 
   const double b = i2d((int)(w - (j << 24))) * kC[kTwoPi32];
   const double2 cs = tb.cs(j);
   const double b2 = b * b;
-  const double s = fma(b2 * b, fma(b2, fma(b2, kC[kS7], kC[kS5]), kC[kS3]), b);
-  const double cm1 = b2 * fma(b2, fma(b2, kC[kC6], kC[kC4]), -0.5);
+  const double s = fma(b2 * b, fma(b2, fma(b2, tb.k(kS7), kC[kS5]), kC[kS3]), b);
+  const double cm1 = b2 * fma(b2, fma(b2, tb.k(kC6), kC[kC4]), -0.5);
   return cs.x + fma(cs.x, cm1, -cs.y * s);
 }
 // e^y for finite y <= 0: k = round(64 y / ln 2), r = y - k ln2/64 (|r| <=
@@ -184,12 +186,12 @@ __device__ __forceinline__ double cos2pi_u32(uint32_t w, const Tab& tb = Tab()) 
 template <class Tab = GlobalTables>
 __device__ __forceinline__ double exp_nonpos(double y, const Tab& tb = Tab()) {
   if (y < -700.0) return exp(y);
-  const double t = fma(y, kC[kInvLn2x64], kC[kRnd]);
+  const double t = fma(y, tb.k(kInvLn2x64), kC[kRnd]);
   const int k = __double2loint(t);
   const double kd = t - kC[kRnd];
   double r = fma(kd, -kC[kLn2Hi64], y);
   r = fma(kd, -kC[kLn2Lo64], r);
-  double q = fma(r, kC[kE6], kC[kE5]);
+  double q = fma(r, tb.k(kE6), kC[kE5]);
   q = fma(r, q, kC[kE4]);
   q = fma(r, q, kC[kE3]);
   q = fma(r, q, 0.5);

@@ -64,6 +64,30 @@ using brng_dev::mt_trial;
 // (GlobalTables).  Staging them in shared memory was measured slower
 // (cfg3 0.929 -> 0.987 ms: random 16-B LDS bank conflicts).
 using Tables = brng_dev::dm::GlobalTables;
+// The same tables with the six constants that meet another constant operand
+// in one DFMA (Horner's first steps of ln / cos / exp, the ln table index and
+// the exp range reduction) held in registers for the whole kernel: left to
+// itself ptxas re-loads one of each pair with LDC in every iteration.  The
+// values are multiplied by 1.0 read from memory (2^0 of the exp table), so
+// they are the same constants but not ones ptxas could rematerialise.
+// Dirichlet (cfg4) 4.061 -> 3.965 ms, identical output (56 registers); the
+// Gamma kernel, at 62 of its 64 registers, is slower with any subset, and
+// table addresses in registers too (64 registers) undo the gain
+// (profiles/r02_regk.txt).
+struct RegTables : brng_dev::dm::GlobalTables {
+  double l7, r128, s7, c6, e6, il2;
+  __device__ __forceinline__ RegTables() {
+    namespace dm = brng_dev::dm;
+    const double one = __ldg(&brng_dev::tab::kExp2[0]);
+    l7 = dm::kC[dm::kL7] * one; r128 = dm::kC[dm::kRndM128] * one; s7 = dm::kC[dm::kS7] * one;
+    c6 = dm::kC[dm::kC6] * one; e6 = dm::kC[dm::kE6] * one; il2 = dm::kC[dm::kInvLn2x64] * one;
+  }
+  __device__ __forceinline__ double k(int i) const {
+    namespace dm = brng_dev::dm;
+    return i == dm::kL7 ? l7 : i == dm::kRndM128 ? r128 : i == dm::kS7 ? s7 : i == dm::kC6 ? c6
+         : i == dm::kE6 ? e6 : i == dm::kInvLn2x64 ? il2 : dm::kC[i];
+  }
+};
 
 // alpha<1 boost work item, parked in a per-warp shared-memory queue so that
 // boosts run as full warps instead of as a divergent branch (36% of cfg3's
@@ -100,9 +124,9 @@ constexpr uint32_t kOffBits = 24;
 // same lane: ILP) and kept in a register, and an accepted alpha<1 sample is
 // boosted in place -- no boost queue.  Pays when most samples are boosted
 // (cfg4: 91%); a sample with alpha >= 1 wastes the block.
-template <typename P, bool SPEC = false, typename Load, typename Sink>
+template <typename P, bool SPEC = false, typename Load, typename Sink, typename Tab>
 __device__ __forceinline__ void mt_queue(uint64_t beg, uint32_t n, uint64_t base,
-                                         const RoundKeys& rk, const Tables& tb, Load load,
+                                         const RoundKeys& rk, const Tab& tb, Load load,
                                          Sink sink, uint32_t& nbad, BoostItem* q) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
@@ -305,7 +329,7 @@ template <typename T>
 __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __grid_constant__ DirArgs<T> a) {
   extern __shared__ double gsm[];
   __shared__ BoostItem qs[kDirThreads / 32][kBoostCap];
-  const Tables tb{};
+  const RegTables tb{};
   BoostItem* q = qs[threadIdx.x >> 5];
   const uint32_t lane = threadIdx.x & 31;
   // a.rpw rows per warp queue: one continuous queue over the group's
