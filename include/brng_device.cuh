@@ -202,15 +202,17 @@ __device__ __forceinline__ double exp_nonpos(double y, const Tab& tb = Tab()) {
 }
 // 1/sqrt(x) for a positive normal x: MUFU.RSQ64H seed (~2^-22) and one
 // cubic Newton step y (1 + e/2 + 3e^2/8), e = 1 - x y^2: ~1 ulp.
-__device__ __forceinline__ double rsqrt_pos(double x) {
+template <class Tab = GlobalTables>
+__device__ __forceinline__ double rsqrt_pos(double x, const Tab& tb = Tab()) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double e = fma(-x * y, y, 1.0);
-  return fma(y * e, fma(e, kC[kNewton3], 0.5), y);
+  return fma(y * e, fma(e, tb.k(kNewton3), 0.5), y);
 }
 // sqrt(x) for x = 0 or a positive normal: x * rsqrt(x) (~2 ulp).
-__device__ __forceinline__ double sqrt_nonneg(double x) {
-  return x > 0.0 ? x * rsqrt_pos(x) : 0.0;
+template <class Tab = GlobalTables>
+__device__ __forceinline__ double sqrt_nonneg(double x, const Tab& tb = Tab()) {
+  return x > 0.0 ? x * rsqrt_pos(x, tb) : 0.0;
 }
 // ln x in binary32 by MUFU.LG2 (flushes subnormal x to 0 -> -inf).  Error
 // <= 2^-22 ln2 absolute for x in [1/2, 2], else <= 2 ulp of log2 x.
@@ -295,10 +297,12 @@ __device__ __forceinline__ void box_muller_f64(uint4 w, double* z0, double* z1,
 
 // ---- Marsaglia-Tsang trial (R-08, R-09) -----------------------------------------
 // d = alpha' - 1/3, c = 1/sqrt(9 d) (~1 ulp).
-__device__ __forceinline__ void mt_consts(double alpha, double& d, double& c) {
+template <class Tab = dm::GlobalTables>
+__device__ __forceinline__ void mt_consts(double alpha, double& d, double& c,
+                                          const Tab& tb = Tab()) {
   const double ap = alpha < 1.0 ? alpha + 1.0 : alpha;
   d = ap - dm::kC[dm::kThird];
-  c = dm::rsqrt_pos(9.0 * d);
+  c = dm::rsqrt_pos(9.0 * d, tb);
 }
 // The binary32 screen of the acceptance test (see mt_trial): +1 accept,
 // -1 reject, 0 = margin inside the error band (decide with mt_exact).
@@ -343,12 +347,14 @@ __device__ __forceinline__ bool mt_exact(double z, double d, double v, uint32_t 
 template <class Tab = dm::GlobalTables>
 __device__ __forceinline__ double mt_normal(uint4 w, const Tab& tb = Tab()) {
   const double L = dm::ln_pos(dm::one_minus_u53(w.x, w.y), tb);
-  return __dmul_rn(dm::sqrt_nonneg(-2.0 * L), dm::cos2pi_u32(w.z, tb));
+  return __dmul_rn(dm::sqrt_nonneg(-2.0 * L, tb), dm::cos2pi_u32(w.z, tb));
 }
+template <class Tab = dm::GlobalTables>
 __device__ __forceinline__ bool mt_accept_z(double z, uint32_t w3, double alpha, double& d,
-                                            double& g) {
+                                            double& g,
+                                            const Tab& tb = Tab()) {
   double c;
-  mt_consts(alpha, d, c);
+  mt_consts(alpha, d, c, tb);
   const double cz = __dmul_rn(c, z);
   const double t = __dadd_rn(1.0, cz);
   if (!(t > 0.0)) return false;
@@ -361,7 +367,7 @@ __device__ __forceinline__ bool mt_accept_z(double z, uint32_t w3, double alpha,
 template <class Tab = dm::GlobalTables>
 __device__ __forceinline__ bool mt_trial(uint4 w, double alpha, double& d, double& g,
                                          const Tab& tb = Tab()) {
-  return mt_accept_z(mt_normal(w, tb), w.w, alpha, d, g);
+  return mt_accept_z(mt_normal(w, tb), w.w, alpha, d, g, tb);
 }
 // ln(1 - u53(w0, w1)) of the boost block: the parameter-free part of the boost
 // (the paper's log-uniform buffer)

@@ -72,7 +72,8 @@ using Tables = brng_dev::dm::GlobalTables;
 // they are the same constants but not ones ptxas could rematerialise.
 // Dirichlet (cfg4) 4.061 -> 3.965 ms, identical output (56 registers); the
 // Gamma kernel, at 62 of its 64 registers, is slower with any subset, and
-// table addresses in registers too (64 registers) undo the gain
+// table addresses or the rsqrt Newton constant in registers too (64
+// registers) undo the gain
 // (profiles/r02_regk.txt).
 struct RegTables : brng_dev::dm::GlobalTables {
   double l7, r128, s7, c6, e6, il2;
