@@ -102,7 +102,7 @@ namespace brng_dev {
 namespace dm {
 enum {
   kL7, kL6, kL5, kL4, kL3, kL2,          // ln: 1/7, -1/6, 1/5, -1/4, 1/3, -1/2
-  kLn2Hi, kLn2Lo, kRndM128, kI2dBias,    // ln 2 split; 1.5*2^52 - 128; 2^52 + 2^31
+  kLn2Hi, kLn2Lo, kRndM128,              // ln 2 split; 1.5*2^52 - 128
   kS7, kS5, kS3, kC6, kC4, kTwoPi32,     // sin/cos Taylor; 2 pi / 2^32
   kE6, kE5, kE4, kE3, kInvLn2x64, kLn2Hi64, kLn2Lo64, kRnd,
   kNewton3, kThird,                      // 3/8 (rsqrt step); 1/3 (M-T d)
@@ -112,7 +112,7 @@ static __constant__ double kC[kNumConst] = {
     1.0 / 7.0, -1.0 / 6.0, 0.2, -0.25, 1.0 / 3.0, -0.5,
     0x1.62e42feep-1,                 // 32 significant bits: e * ln2_hi is exact
     0x1.a39ef35793c76p-33,           // ln 2 - ln2_hi
-    6755399441055744.0 - 128.0, 4503599627370496.0 + 2147483648.0,
+    6755399441055744.0 - 128.0,
     -1.0 / 5040.0, 1.0 / 120.0, -1.0 / 6.0, -1.0 / 720.0, 1.0 / 24.0,
     0x1.921fb54442d18p-30,           // 2 pi / 2^32
     1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0,
@@ -132,10 +132,12 @@ struct GlobalTables {
   __device__ __forceinline__ double2 cs(uint32_t j) const { return __ldg(&tab::kCos[j]); }
   __device__ __forceinline__ double exp2(int j) const { return __ldg(&tab::kExp2[j]); }
 };
-// exact binary64 of a 32-bit signed integer without the I2F pipe
-__device__ __forceinline__ double i2d(int v) {
-  return __hiloint2double(0x43300000, v ^ (int)0x80000000) - kC[kI2dBias];
-}
+// exact binary64 of a 32-bit signed integer: one I2F.F64.S32 (XU pipe).  The
+// bit-built form (2^52 + 2^31 + v) - (2^52 + 2^31) -- the same values -- took
+// an IMAD.MOV of the constant high word, a LOP3 and a DADD per use: Gamma
+// 0.830 -> 0.820 ms and Dirichlet 3.964 -> 3.915 ms with the conversion
+// (identical outputs; profiles/r02_i2d.txt).
+__device__ __forceinline__ double i2d(int v) { return (double)v; }
 // 1 - u53(lo, hi), exactly, from the bits: with k = (hi:lo) >> 11 (53 bits),
 // D = 2^52 + (k mod 2^52) and t = bit 52 of k, 1 - k 2^-53 = (t ? 1 : 1.5) -
 // D 2^-53 (one exact FMA; no integer->double conversion).
