@@ -141,7 +141,6 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint32_t n, uint64_t base
   // that F2F.F64.F32, ncu source view)
   P alpha_r = P(1), beta_r = P(1);
   double d = 0.0;
-  double Lb = 0.0;                                   // SPEC: boost ln(1-u) of the lane's sample
   uint32_t t = 1;
   uint32_t qn = 0;                                   // queued boosts (warp-uniform)
   // issue the parameter loads only; they are consumed after the next trial's
@@ -175,34 +174,47 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint32_t n, uint64_t base
     bool done = false, boost = false;
     double g = 0.0;
     double alpha = 1.0;
+    double Lb = 0.0;                                 // SPEC: boost ln(1-u) of the sample
     if (active) {
       const uint64_t pos = base_c + ((uint64_t)off << 8);   // kStride = 256 blocks per sample
       const uint4 w = philox_block_rk(pos + t, rk);
       if (SPEC) {
-        // every lane computes it, kept from trial 1: no divergent region
-        // (retrying lanes would idle through it anyway): cfg4 4.160 -> 4.052 ms
-        const double Ln = brng_dev::mt_boost_log(philox_block_rk(pos, rk), tb);
-        Lb = t == 1 ? Ln : Lb;
+        // every lane computes it from trial 1 on: no divergent region
+        // (retrying lanes would idle through it anyway): cfg4 4.160 ->
+        // 4.052 ms.  The boost block does not depend on t, so every trial
+        // gets the same value (no select of the trial-1 value: 3.902 ->
+        // 3.878 ms, profiles/r02_queue_decision.txt).
+        Lb = brng_dev::mt_boost_log(philox_block_rk(pos, rk), tb);
       }
       alpha = (double)alpha_r;
       const double beta = (double)beta_r;
       const bool valid = isfinite(alpha) && isfinite(beta) && alpha > 0.0 && beta > 0.0;
       const bool acc = mt_trial(w, alpha, d, g, tb);
-      if (!valid) {
-        done = true; t = 0; ++nbad;
-      } else if (acc) {
-        done = true;
-      } else if (++t > kMaxTrial) {
-        done = true; t = 0; ++nbad;
-      }
-      boost = done && t != 0 && alpha < 1.0;
       if (SPEC) {
+        // the decision as predicates (the same outcomes as the branch chain
+        // below), one select for the boost and one for the stored value:
+        // 3.878 -> 3.817-3.832 ms; the Gamma queue is slower this way
+        // (0.817 -> 0.834 ms) and keeps the chain
+        const uint32_t tn = t + 1u;
+        const bool cap = !acc & (tn > kMaxTrial);
+        const bool fail = !valid | cap;
+        done = !valid | acc | cap;
+        t = fail ? 0u : (acc ? t : tn);
+        nbad += fail ? 1u : 0u;
+        const bool bst = (!fail & acc) & (alpha < 1.0);
         const double gb = brng_dev::mt_boost_from_log(Lb, g, alpha, tb);
-        g = boost ? gb : g;
-        if (done) sink(off, t != 0 ? g * beta : qnan(), t);
-        boost = false;
-      } else if (done && !boost) {
-        sink(off, t != 0 ? g * beta : qnan(), t);
+        const double gv = bst ? gb : g;
+        if (done) sink(off, fail ? qnan() : gv * beta, t);
+      } else {
+        if (!valid) {
+          done = true; t = 0; ++nbad;
+        } else if (acc) {
+          done = true;
+        } else if (++t > kMaxTrial) {
+          done = true; t = 0; ++nbad;
+        }
+        boost = done && t != 0 && alpha < 1.0;
+        if (done && !boost) sink(off, t != 0 ? g * beta : qnan(), t);
       }
     }
     const uint32_t bm = SPEC ? 0u : __ballot_sync(kFull, boost);
