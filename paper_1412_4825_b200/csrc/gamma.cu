@@ -45,8 +45,8 @@ __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000
 // optimiser, so a sample's address is one IMAD.WIDE.U32 (offset x size +
 // pointer) instead of a re-derived 64-bit (chunk start + offset) sum, shift
 // and add per access: Gamma cfg3 0.839-0.847 -> 0.825-0.828 ms, identical
-// output; the Dirichlet queue is no faster with it (4.058 vs 4.062-4.067 ms,
-// profiles/r02_opaque_ptr.txt) and keeps plain pointers.
+// output (profiles/r02_opaque_ptr.txt; the Dirichlet queue gained from it only
+// after its other round-2 changes, profiles/r02_dir_addr.txt).
 template <typename T>
 __device__ __forceinline__ T* chunk_ptr(T* p) {
   asm("mov.b64 %0, %0;" : "+l"(p));
@@ -258,10 +258,12 @@ struct GammaArgs {
 #ifndef BRNG_GAMMA_DYN
 #define BRNG_GAMMA_DYN 1
 #endif
-template <typename T>
 #ifndef BRNG_GAMMA_MINB
 #define BRNG_GAMMA_MINB 4
 #endif
+// TR: the call passed a trials array (a compile-time branch: without one the
+// queue's sink has no per-sample null test and address arithmetic for it)
+template <typename T, bool TR>
 __global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(const __grid_constant__ GammaArgs<T> a) {
   __shared__ BoostItem qs[kThreads / 32][kBoostCap];
   const Tables tb{};
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(const 
     const T* al_c = chunk_ptr(a.alpha + beg);
     const T* be_c = chunk_ptr(a.beta + beg);
     T* out_c = chunk_ptr(a.out + beg);
-    uint8_t* tr_c = a.trials ? chunk_ptr(a.trials + beg) : nullptr;
+    uint8_t* tr_c = TR ? chunk_ptr(a.trials + beg) : nullptr;
     mt_queue<T, BRNG_GAMMA_SPEC != 0>(
         beg, n, a.base, a.rk, tb,
         [&](uint32_t o, T& al, T& be) {
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, BRNG_GAMMA_MINB) gamma_kernel(const 
         },
         [&](uint32_t o, double v, uint32_t t) {
           out_c[o] = (T)v;
-          if (tr_c) tr_c[o] = (uint8_t)t;
+          if (TR) tr_c[o] = (uint8_t)t;
         },
         nbad, q);
   }
@@ -338,7 +340,7 @@ __device__ __forceinline__ double warp_sum(double s) {
 // K <= kDirSmemK: Gammas of the row staged in shared memory (8 K bytes/warp),
 // summed lane-strided then by a fixed xor-shuffle tree, normalised, stored
 // coalesced.
-template <typename T>
+template <typename T, bool TR>
 __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __grid_constant__ DirArgs<T> a) {
   extern __shared__ double gsm[];
   __shared__ BoostItem qs[kDirThreads / 32][kBoostCap];
@@ -366,8 +368,13 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __gri
     const uint64_t row0 = grp * a.rpw;
     const uint64_t rows = a.n_rows - row0 < a.rpw ? a.n_rows - row0 : a.rpw;
     const uint64_t beg = row0 * a.k;
-    const T* al_c = a.alpha + beg;
-    uint8_t* tr_c = a.trials ? a.trials + beg : nullptr;
+    // the chunk pointer behind an empty asm (one IMAD.WIDE per address, as in
+    // the Gamma kernel) and the staging row as a 32-bit shared address
+    // (no per-store generic-to-shared window arithmetic): 3.811 -> 3.737-3.743
+    // ms together (profiles/r02_dir_addr.txt)
+    const T* al_c = chunk_ptr(a.alpha + beg);
+    uint8_t* tr_c = TR ? a.trials + beg : nullptr;
+    const uint32_t g_sh = (uint32_t)__cvta_generic_to_shared(g_grp);
     mt_queue<T, BRNG_DIR_SPEC != 0>(
         beg, (uint32_t)(rows * a.k), a.base, a.rk, tb,
         [&](uint32_t o, T& al, T& be) {
@@ -375,8 +382,8 @@ __global__ void __launch_bounds__(kDirThreads) dirichlet_smem_kernel(const __gri
           be = T(1);
         },
         [&](uint32_t o, double v, uint32_t t) {
-          g_grp[o] = v;
-          if (tr_c) tr_c[o] = (uint8_t)t;
+          asm volatile("st.shared.f64 [%0], %1;" ::"r"(g_sh + 8u * o), "d"(v) : "memory");
+          if (TR) tr_c[o] = (uint8_t)t;
         },
         nbad, q);
     __syncwarp();
@@ -494,7 +501,10 @@ cudaError_t gamma_typed(const T* alpha, const T* beta, T* out, uint8_t* trials, 
   const uint64_t cap = (uint64_t)ctx.num_sms * 8;  // two waves of 4 resident CTAs/SM
 #endif
   const unsigned g = (unsigned)(ctas_needed < cap ? ctas_needed : cap);
-  gamma_kernel<T><<<g, kThreads, 0, ctx.stream>>>(a);
+  if (a.trials)
+    gamma_kernel<T, true><<<g, kThreads, 0, ctx.stream>>>(a);
+  else
+    gamma_kernel<T, false><<<g, kThreads, 0, ctx.stream>>>(a);
   return cudaGetLastError();
 }
 
@@ -528,9 +538,12 @@ cudaError_t dirichlet_typed(const T* alpha, uint64_t n_rows, uint64_t k, T* out,
     a.rpw = (uint32_t)(r < 1 ? 1 : (r > 8 ? 8 : r));
     const size_t smem = (size_t)4 * a.rpw * k * sizeof(double);
     if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(dirichlet_smem_kernel<T>,
+      cudaError_t e = cudaFuncSetAttribute(dirichlet_smem_kernel<T, true>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(dirichlet_smem_kernel<T, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
     }
     const uint64_t groups = (n_rows + a.rpw - 1) / a.rpw;
@@ -538,8 +551,9 @@ cudaError_t dirichlet_typed(const T* alpha, uint64_t n_rows, uint64_t k, T* out,
 #if BRNG_GAMMA_DYN
     // one resident wave of CTAs; warps take row groups from a counter
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dirichlet_smem_kernel<T>,
-                                                      kDirThreads, smem) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, trials ? dirichlet_smem_kernel<T, true> : dirichlet_smem_kernel<T, false>,
+            kDirThreads, smem) != cudaSuccess ||
         per_sm < 1)
       per_sm = 1;
     const uint64_t cap = (uint64_t)ctx.num_sms * per_sm;
@@ -549,7 +563,10 @@ cudaError_t dirichlet_typed(const T* alpha, uint64_t n_rows, uint64_t k, T* out,
     const uint64_t cap = (uint64_t)ctx.num_sms * 16 * 8;
 #endif
     const unsigned g = (unsigned)(ctas < cap ? ctas : cap);
-    dirichlet_smem_kernel<T><<<g, kDirThreads, smem, ctx.stream>>>(a);
+    if (trials)
+      dirichlet_smem_kernel<T, true><<<g, kDirThreads, smem, ctx.stream>>>(a);
+    else
+      dirichlet_smem_kernel<T, false><<<g, kDirThreads, smem, ctx.stream>>>(a);
   } else {
     uint64_t cap = (uint64_t)ctx.num_sms * 16 * 8;
     if (sizeof(T) == 4 && ctx.dir_scratch) {
