@@ -193,6 +193,11 @@ template <bool STORE, bool STATS, int CPT, int UNROLL, bool UHI>
 __device__ __forceinline__ void sweeps(const GibbsArgs& a, const RoundKeys& rk, uint32_t s_begin,
                                        uint32_t s_end, Chain (&ch)[CPT], uint32_t hist_base) {
   uint32_t s = s_begin;
+  // -2^-64 multiplied by a 1.0 read from memory: the same constant, but one
+  // ptxas keeps in a register instead of rematerialising it with two
+  // IMAD.MOVs (FMA pipe) in every unrolled iteration: cfg5 183.5 -> 181.95 ms,
+  // identical output (profiles/r02_gibbs_pin.txt)
+  const double ninv = -kInvScale * __ldg(&brng_dev::tab::kExp2[0]);
   while (s < s_end) {
     const uint64_t pos = a.base + s;
     const uint32_t pos_lo = (uint32_t)pos;
@@ -211,8 +216,8 @@ __device__ __forceinline__ void sweeps(const GibbsArgs& a, const RoundKeys& rk, 
         Chain& q = ch[k];
         const uint4 w = UHI ? chain_block_u(ck[k], p0, p1u, rk) : chain_block(ck[k], p0, rk);
         // x = fl(fl(1-y) u53)  <=>  X = fl(fl(1-y) u53 2^64),  1-y = fma(Y, -2^-64, 1)
-        q.X = __dmul_rn(__fma_rn(q.Y, -kInvScale, 1.0), u53_scaled(w.x, w.y));
-        q.Y = __dmul_rn(__fma_rn(q.X, -kInvScale, 1.0), u53_scaled(w.z, w.w));
+        q.X = __dmul_rn(__fma_rn(q.Y, ninv, 1.0), u53_scaled(w.x, w.y));
+        q.Y = __dmul_rn(__fma_rn(q.X, ninv, 1.0), u53_scaled(w.z, w.w));
         if (STORE && q.live) {
           if (a.out_x) a.out_x[(uint64_t)s * a.n_chains + q.c] = __dmul_rn(q.X, kInvScale);
           if (a.out_y) a.out_y[(uint64_t)s * a.n_chains + q.c] = __dmul_rn(q.Y, kInvScale);
