@@ -81,20 +81,21 @@ __device__ __forceinline__ double u53_scaled(uint32_t lo, uint32_t hi) {
   return __ull2double_rn(((uint64_t)hi << 32) | (lo & 0xFFFFF800u));
 }
 
-// floor(256 x) = floor(X 2^-56) for X = x 2^64 in [0, 2^64): with E the
-// unbiased exponent of X, the bin is the top E-55 bits of 1.mantissa, all in
-// the high word; E < 56 (and X = 0) shift everything out (shift >= 21; PTX
-// shr clamps shifts >= 32 to a zero result).
-// Shared address of X's histogram counter: base | 4 floor(256 x), with base
-// 1024-aligned (a live chain's histogram, or the sink of a dead chain).  The
-// shift by two less yields 4 bin + 2 stray low bits, cleared by the same LOP3
-// that ORs the base in: all ALU-pipe work (no IMAD.SHL / IMAD.MOV on the
-// FMA-heavy pipe).
+// floor(256 x) = floor(X 2^-56) for X = x 2^64 in [0, 2^64): X's integer
+// part, exact, by one F2I.U64.F64.TRUNC on the XU pipe; its bits 63..56 are
+// the bin (X = 0 and tiny X give 0; a dead chain's NaN converts to 0 and
+// counts into the sink).  Shared address of the counter: base | 4 bin, base
+// 1024-aligned (a live chain's histogram, or the sink of a dead chain): the
+// high word shifted by 22 is 4 bin + 2 stray low bits, cleared by the LOP3
+// that ORs the base in.  Round 1 read the bin from the exponent and mantissa
+// bits with five ALU operations to stay off the FMA pipe; the conversion is
+// the same value with three instructions fewer per chain-sweep and the XU
+// pipe has the room: cfg5 181.96 -> 177.17 ms, identical histograms
+// (profiles/r02_gibbs_bin.txt).
 __device__ __forceinline__ uint32_t bin_addr_scaled(double X, uint32_t base) {
-  const uint32_t h = (uint32_t)__double2hiint(X);
-  const uint32_t sh = 1097u - (h >> 20);
+  const uint32_t h64 = (uint32_t)(__double2ull_rz(X) >> 32);
   uint32_t b;
-  asm("shr.b32 %0, %1, %2;" : "=r"(b) : "r"((h & 0xFFFFFu) | 0x100000u), "r"(sh));
+  asm("shr.b32 %0, %1, 22;" : "=r"(b) : "r"(h64));
   return (b & 0x3FCu) | base;
 }
 
