@@ -152,11 +152,11 @@ __device__ __forceinline__ double one_minus_u53(uint32_t lo, uint32_t hi) {
 // 0.0056); ln x = e ln2 - ln c_j + log1p(r), log1p by its Taylor series to
 // r^7.  c_0 = 1 and ln c_0 = 0, so for x near 1 the result is log1p(x-1)
 // to ~1 ulp relative.
+// ln of the positive normal binary64 with high word hx and low word lx
 template <class Tab = GlobalTables>
-__device__ __forceinline__ double ln_pos(double x, const Tab& tb = Tab()) {
-  const int hx = __double2hiint(x);
+__device__ __forceinline__ double ln_pos_bits(int hx, int lx, const Tab& tb = Tab()) {
   const int e = (hx - 0x3FE6A09E) >> 20;
-  const double m = __hiloint2double(hx - e * (1 << 20), __double2loint(x));
+  const double m = __hiloint2double(hx - e * (1 << 20), lx);
   const int j = __double2loint(fma(m, 128.0, tb.k(kRndM128)));
   const double2 ct = tb.ln(j + tab::kLnOff);
   const double r = fma(m, ct.x, -1.0);
@@ -168,6 +168,10 @@ __device__ __forceinline__ double ln_pos(double x, const Tab& tb = Tab()) {
   const double de = i2d(e);
   const double lo = fma(r * r, q, de * kC[kLn2Lo]) + r;
   return fma(de, kC[kLn2Hi], ct.y) + lo;
+}
+template <class Tab = GlobalTables>
+__device__ __forceinline__ double ln_pos(double x, const Tab& tb = Tab()) {
+  return ln_pos_bits(__double2hiint(x), __double2loint(x), tb);
 }
 // cos(2 pi w 2^-32): j = round(w / 2^24) mod 256, b = 2 pi (w - j 2^24) 2^-32
 // (|b| <= pi/256); cos(a_j + b) = C_j cos b - S_j sin b with Taylor cos b - 1
@@ -261,9 +265,16 @@ __device__ __forceinline__ void sincos2pi_u53(uint32_t lo, uint32_t hi, double* 
   *sn = t.y + fma(t.y, cm1, t.x * sb);
 }
 // ln(1 - u53(lo, hi)) (<= 0; exact 0 at u = 0)
+// 1 - u53 = N 2^-53 with N = 2^53 - k (k the 53-bit integer of the words),
+// exact: N is converted by one I2F.F64.U64 (XU pipe) and the 2^-53 applied to
+// its exponent field -- the same binary64 value as one_minus_u53, without its
+// DFMA and the constant's zero low word (Gamma 0.815 -> 0.807 ms, Dirichlet
+// 3.735 -> 3.693 ms, identical outputs; profiles/r02_ln1m.txt)
 template <class Tab = GlobalTables>
 __device__ __forceinline__ double ln1m_u53(uint32_t lo, uint32_t hi, const Tab& tb = Tab()) {
-  return ln_pos(one_minus_u53(lo, hi), tb);
+  const uint64_t k = (((uint64_t)hi << 32) | lo) >> 11;
+  const double D = __ull2double_rn((1ull << 53) - k);
+  return ln_pos_bits(__double2hiint(D) - (53 << 20), __double2loint(D), tb);
 }
 // e^y for |y| <= 700 by the table path of exp_nonpos (positive k scales the
 // exponent up, no overflow below 709); libdevice beyond.
@@ -348,7 +359,7 @@ __device__ __forceinline__ bool mt_exact(double z, double d, double v, uint32_t 
 // reading R-33) computes the same decision and value bit for bit.
 template <class Tab = dm::GlobalTables>
 __device__ __forceinline__ double mt_normal(uint4 w, const Tab& tb = Tab()) {
-  const double L = dm::ln_pos(dm::one_minus_u53(w.x, w.y), tb);
+  const double L = dm::ln1m_u53(w.x, w.y, tb);
   return __dmul_rn(dm::sqrt_nonneg(-2.0 * L, tb), dm::cos2pi_u32(w.z, tb));
 }
 template <class Tab = dm::GlobalTables>
@@ -375,7 +386,7 @@ __device__ __forceinline__ bool mt_trial(uint4 w, double alpha, double& d, doubl
 // (the paper's log-uniform buffer)
 template <class Tab = dm::GlobalTables>
 __device__ __forceinline__ double mt_boost_log(uint4 wb, const Tab& tb = Tab()) {
-  return dm::ln_pos(dm::one_minus_u53(wb.x, wb.y), tb);
+  return dm::ln1m_u53(wb.x, wb.y, tb);
 }
 template <class Tab = dm::GlobalTables>
 __device__ __forceinline__ double mt_boost_from_log(double L, double g, double alpha,
