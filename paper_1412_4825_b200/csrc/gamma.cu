@@ -93,10 +93,13 @@ struct RegTables : brng_dev::dm::GlobalTables {
 // alpha<1 boost work item, parked in a per-warp shared-memory queue so that
 // boosts run as full warps instead of as a divergent branch (36% of cfg3's
 // samples, 91% of cfg4's).
-// 16 bytes: the boost re-reads the sample's alpha, beta (just loaded, so
-// cache hits), which halves the queue's shared memory (occupancy).
+// 32 bytes with the sample's alpha and beta (BRNG_SLIM_QUEUE=1: 16 bytes,
+// the drain re-reading them from global memory).  The slim item was chosen in
+// round 1 to halve the queue's shared memory; at 4 CTAs/SM the full item
+// costs 16 KB per CTA and saves the drain's two loads and their address
+// arithmetic: cfg3 0.801 -> 0.789 ms, identical output (profiles/r02_queue_item.txt).
 #ifndef BRNG_SLIM_QUEUE
-#define BRNG_SLIM_QUEUE 1
+#define BRNG_SLIM_QUEUE 0
 #endif
 struct BoostItem {
   double g;
