@@ -92,7 +92,7 @@ __global__ void k_gibbs(uint64_t seed, uint64_t stream_id, uint64_t base, uint64
 // function per `fn`: 0 ln_pos(x), 1 cos2pi_u32(w), 2 exp_nonpos(x),
 // 3 one_minus_u53(w[2i], w[2i+1]), 4 rsqrt_pos(x), 5 sqrt_nonneg(x),
 // 6/7 sin/cos of sincos2pi_u24(w) (binary32), 8/9 sin/cos of
-// sincos2pi_u53(w[2i], w[2i+1]), 10 exp_small(x).
+// sincos2pi_u53(w[2i], w[2i+1]), 10 exp_small(x), 11/12 ln(1 - u53) two ways.
 __global__ void k_math(int fn, const double* x, const uint32_t* w, double* out, uint64_t n) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -115,6 +115,10 @@ __global__ void k_math(int fn, const double* x, const uint32_t* w, double* out, 
     out[i] = fn == 8 ? sn : cs;
   }
   if (fn == 10) out[i] = dm::exp_small(x[i]);
+  // 11 ln1m_u53 (1 - u53 converted by I2F, exponent adjusted), 12 the same
+  // value through the bit-built one_minus_u53 and ln_pos
+  if (fn == 11) out[i] = dm::ln1m_u53(w[2 * i], w[2 * i + 1]);
+  if (fn == 12) out[i] = dm::ln_pos(dm::one_minus_u53(w[2 * i], w[2 * i + 1]));
 }
 // The Marsaglia-Tsang decision pieces on given Philox words: the binary32
 // screen (+1/-1/0) and the exact binary64 test, for trials with 1 + cz > 0

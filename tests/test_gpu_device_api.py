@@ -234,6 +234,28 @@ def test_dm_one_minus_u53_exact(user_lib):
         assert float(g) == (2**53 - k) / 2**53, (lo, hi)
 
 
+def test_dm_ln1m_u53_two_paths_and_accuracy(user_lib):
+    """ln(1 - u53) as the kernels compute it (1 - u53 = (2^53 - k) 2^-53 by
+    I2F, 53 taken off the exponent) equals ln_pos(one_minus_u53(...)) bit for
+    bit, is exactly 0 at k = 0, and is within 2.5 ulp of mpmath."""
+    import mpmath as mp
+    mp.mp.dps = 40
+    rng = np.random.default_rng(14)
+    pairs = [(0, 0), (0x800, 0), (0, 0x80000000), (0xFFFFFFFF, 0xFFFFFFFF), (0x7FF, 0),
+             (0xFFFFF800, 0x7FFFFFFF), (0, 0x00100000), (0xFFFFF800, 0xFFFFFFFF)]
+    pairs += [tuple(int(v) for v in rng.integers(0, 2**32, 2, dtype=np.uint64))
+              for _ in range(4000)]
+    w = [v for p in pairs for v in p]
+    a = _math(user_lib, 11, w=w, n=len(pairs))
+    b = _math(user_lib, 12, w=w, n=len(pairs))
+    assert np.array_equal(np.asarray(a).view(np.uint64), np.asarray(b).view(np.uint64))
+    assert a[0] == 0.0
+    exact = [mp.log(mp.mpf(2**53 - (((hi << 32) | lo) >> 11)) / mp.mpf(2) ** 53)
+             for lo, hi in pairs]
+    err = _ulp_err(a, exact)
+    assert max(err) <= 2.5, max(err)
+
+
 def test_dm_rsqrt_sqrt_accuracy(user_lib):
     """rsqrt_pos within 1.5 ulp and sqrt_nonneg within 2.5 ulp of mpmath on
     the trial's arguments (9d in [6, 1800], -2 ln(1-u) in [0, 74]) and

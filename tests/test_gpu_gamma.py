@@ -146,6 +146,26 @@ def test_dirichlet_equals_normalised_gamma_counters():
                                rtol=1e-14, atol=1e-300)
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("k", [37, 256, 1500])
+def test_dirichlet_trials_array_does_not_change_values(dtype, k):
+    """The kernels are specialised on whether a trials array was passed (no
+    per-sample null test without one); both forms give the same bits."""
+    rows = 300
+    al = workloads.cfg4_params(rows, k, seed=8).numpy().astype(dtype)
+    td = torch.float32 if dtype == np.float32 else torch.float64
+    fn = B.brng_dirichlet_f32 if dtype == np.float32 else B.brng_dirichlet_f64
+    outs = []
+    for with_trials in (False, True):
+        x = torch.empty(rows, k, dtype=td, device=dev())
+        tr = torch.empty(rows, k, dtype=torch.uint8, device=dev()) if with_trials else None
+        with handle(9, 2, 77) as h:
+            fn(h, torch.from_numpy(al).to(dev()), rows, k, x, tr)
+            assert B.brng_device_errors(h) == 0
+        outs.append(x.cpu().numpy())
+    assert np.array_equal(outs[0].view(np.uint8), outs[1].view(np.uint8))
+
+
 def test_dirichlet_invalid_row():
     alpha = torch.ones(3, 4, dtype=torch.float64)
     alpha[1, 2] = -1.0
