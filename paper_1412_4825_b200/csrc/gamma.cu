@@ -150,9 +150,14 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint32_t n, uint64_t base
   uint32_t qn = 0;                                   // queued boosts (warp-uniform)
   // issue the parameter loads only; they are consumed after the next trial's
   // Philox block and Box-Muller normal
+  // SPEC: the sample's counter base kept from its refill (Dirichlet 3.70 ->
+  // 3.68 ms); the Gamma queue, at its register cap, recomputes it (keeping it
+  // there was 3.5% slower; profiles/r02_recheck.txt)
+  uint64_t pos_r = SPEC ? base_c + ((uint64_t)off << 8) : 0;
   auto setup = [&]() {
     load(off, alpha_r, beta_r);
     t = 1;
+    if (SPEC) pos_r = base_c + ((uint64_t)off << 8);
   };
   // lanes [0, k) take the last k queue entries, boost and sink them
   auto drain = [&](uint32_t k) {
@@ -181,7 +186,7 @@ __device__ __forceinline__ void mt_queue(uint64_t beg, uint32_t n, uint64_t base
     double alpha = 1.0;
     double Lb = 0.0;                                 // SPEC: boost ln(1-u) of the sample
     if (active) {
-      const uint64_t pos = base_c + ((uint64_t)off << 8);   // kStride = 256 blocks per sample
+      const uint64_t pos = SPEC ? pos_r : base_c + ((uint64_t)off << 8);   // 256 blocks per sample
       const uint4 w = philox_block_rk(pos + t, rk);
       if (SPEC) {
         // every lane computes it from trial 1 on: no divergent region
